@@ -1,0 +1,855 @@
+// =============================================================================
+// oracle/oracle.cpp -- the CPU ORACLE for the Vanka / V-cycle / FGMRES hot path
+// of Spies, Olson, MacLachlan, "Exploiting mesh structure to improve multigrid
+// performance for saddle point problems" (arXiv 2401.06277).
+//
+// THIS IS TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, the smoke() of
+// __graft_entry__.py and bench.py's cpu_baseline / --impl reference leg may
+// load it.  It shares no code, header, table or constant generator with the
+// CUDA library under paper_2401_06277_b200/ (and never includes anything from
+// there); the two agree only on the documented vector layout.
+//
+// Deliberately plain and slow: the operator is assembled element by element
+// into an explicit CSR matrix by 3x3 Gauss quadrature of the bilinear forms;
+// every Vanka patch matrix is extracted from that global CSR and solved with a
+// dense LU; the interpolation P is built by evaluating coarse basis functions;
+// the V-cycle and FGMRES follow the paper's algorithms line by line.
+//
+// Citations: P:n = /root/reference/PAPER.md line n (+ label).  Readings where
+// the paper is silent or inconsistent are those of SURVEY.md section 8(c) and
+// are listed in DESIGN.md ("Readings").
+//
+// Vector layout on level with N elements per dimension (all fp64, compact):
+//   [ u_x on the (2N+1)^2 velocity lattice, index j*(2N+1)+i (x fastest),
+//     u_y on the same lattice,
+//     p on the (N+1)^2 pressure nodes, index ky*(N+1)+kx ]
+// lattice point (i,j) sits at (i*h/2, j*h/2); pressure node (kx,ky) at (kx*h, ky*h).
+// Level 0 is the coarsest (alg:mg); level L-1 the finest.
+//
+// parity pins (tests/test_oracle_*.py): brute-force dense NumPy checker for
+// N<=8, nodal exactness of two manufactured solutions, symmetry / null vector,
+// 25 patch groups and tab:rwf counts, Galerkin identity, pinv for the coarse
+// solve, FGMRES against its least-squares definition.  The V-cycle's
+// convergence factor is "parity unpinned" against the paper (the paper prints
+// none) -- it is pinned only by the internal checks above.
+// =============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+struct Csr {
+  int64_t nrows = 0;
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> col;
+  std::vector<double> val;
+};
+
+struct Level {
+  int N = 0;
+  double h = 0;
+  int64_t nlat = 0;  // 2N+1
+  int64_t nv = 0;    // (2N+1)^2 velocity DOFs per component
+  int64_t npn = 0;   // N+1
+  int64_t np = 0;    // (N+1)^2 pressure DOFs
+  int64_t ntot = 0;  // 2 nv + np
+  Csr A;             // full assembled operator [[L, B^T],[B, 0]] (eq:stokesmatrix)
+  std::vector<uint8_t> dir;  // Dirichlet flag per DOF
+  // Vanka (alg:vk)
+  std::vector<int64_t> pstart;  // patch p owns dofs pdof[pstart[p] .. pstart[p+1])
+  std::vector<int64_t> pdof;
+  std::vector<int32_t> pgroup;  // index of the distinct patch matrix (its LU)
+  std::vector<std::vector<double>> glu;  // LU factors of each distinct A_i
+  std::vector<std::vector<int>> gpiv;
+  std::vector<int> gsize;
+  std::vector<double> weight;  // diagonal of W_i, per global DOF (see reading 6)
+  // interpolation from level-1 (coarse) into this level
+  Csr P, PT;
+  // level-0 direct solve (reading 3: minimum-norm)
+  std::vector<int64_t> interior;
+  std::vector<double> clu;
+  std::vector<int> cpiv;
+  int cn = 0;
+};
+
+struct Ctx {
+  double nu = 1.0, omega = 0.8;
+  int weighting = 0;  // 0: W_i = omega*diag(1/mult); 1: W_i = omega*I
+  int nu1 = 1, nu2 = 1;
+  int coarse_mode = 0;  // 0: exact min-norm solve; 1: three Vanka sweeps
+  std::vector<Level> lev;
+  std::string err;
+};
+
+// --------------------------------------------------------------------------
+// 1D Lagrange bases on the reference interval [0,1] (Q2 = biquadratic,
+// Q1 = bilinear tensor-product bases).
+// Quadratic nodes t = 0, 1/2, 1; linear nodes t = 0, 1.
+// --------------------------------------------------------------------------
+double q2(int a, double t) {
+  if (a == 0) return 2.0 * (t - 0.5) * (t - 1.0);
+  if (a == 1) return -4.0 * t * (t - 1.0);
+  return 2.0 * t * (t - 0.5);
+}
+double dq2(int a, double t) {  // d/dt
+  if (a == 0) return 4.0 * t - 3.0;
+  if (a == 1) return -8.0 * t + 4.0;
+  return 4.0 * t - 1.0;
+}
+double q1(int a, double t) { return a == 0 ? 1.0 - t : t; }
+
+// 3-point Gauss-Legendre rule on [0,1]; exact for polynomials of degree <= 5,
+// which covers every integrand of the forms a(.,.), b(.,.) and (f, v) here.
+const double kGP[3] = {0.5 - 0.5 * std::sqrt(0.6), 0.5, 0.5 + 0.5 * std::sqrt(0.6)};
+const double kGW[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+
+// --------------------------------------------------------------------------
+// Right-hand sides / boundary data (P:76-81 manufactured solution; readings
+// 2 and 15 of DESIGN.md for the boundary data and the cavity).
+// kind 0 ZERO, 1 MMS_PAPER, 2 MMS_INSPACE, 3 CAVITY
+// --------------------------------------------------------------------------
+void exact_u(int kind, double x, double y, double* ux, double* uy) {
+  if (kind == 1) {
+    // u = ( x(1-x)(2x-1)(6y^2-6y+1), y(y-1)(2y-1)(6x^2-6x+1) )
+    *ux = x * (1 - x) * (2 * x - 1) * (6 * y * y - 6 * y + 1);
+    *uy = y * (y - 1) * (2 * y - 1) * (6 * x * x - 6 * x + 1);
+  } else if (kind == 2) {
+    *ux = 2 * x * x * y;
+    *uy = -2 * x * y * y;
+  } else {
+    *ux = 0;
+    *uy = 0;
+  }
+}
+void exact_p(int kind, double x, double y, double* p) {
+  if (kind == 1) *p = x * x - 3 * y * y + 8.0 / 3.0 * x * y;
+  else if (kind == 2) *p = x * y - 0.25;
+  else *p = 0;
+}
+// f = -nu Laplace(u) + grad p  (eq:stokes1; "f computed to satisfy")
+void forcing(int kind, double nu, double x, double y, double* fx, double* fy) {
+  if (kind == 1) {
+    // u_x = x(1-x)(2x-1) * (6y^2-6y+1)
+    double gx = x * (1 - x) * (2 * x - 1);        // -2x^3+3x^2-x
+    double gx_xx = -12 * x + 6;                    // d2/dx2
+    double hy = 6 * y * y - 6 * y + 1, hy_yy = 12;
+    double lap_ux = gx_xx * hy + gx * hy_yy;
+    // u_y = y(y-1)(2y-1) * (6x^2-6x+1)
+    double gy = y * (y - 1) * (2 * y - 1);         // 2y^3-3y^2+y
+    double gy_yy = 12 * y - 6;
+    double hx = 6 * x * x - 6 * x + 1, hx_xx = 12;
+    double lap_uy = gy_yy * hx + gy * hx_xx;
+    double px = 2 * x + 8.0 / 3.0 * y, py = -6 * y + 8.0 / 3.0 * x;
+    *fx = -nu * lap_ux + px;
+    *fy = -nu * lap_uy + py;
+  } else if (kind == 2) {
+    // u = (2x^2 y, -2 x y^2): Laplace u = (4y, -4x); p = xy - 1/4: grad p = (y, x)
+    *fx = -nu * 4 * y + y;
+    *fy = nu * 4 * x + x;
+  } else {
+    *fx = 0;
+    *fy = 0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Dense LU with partial pivoting (row-major n x n), and solve.
+// --------------------------------------------------------------------------
+bool lu_factor(std::vector<double>& a, std::vector<int>& piv, int n) {
+  piv.resize(n);
+  for (int k = 0; k < n; ++k) {
+    int pr = k;
+    double best = std::fabs(a[(size_t)k * n + k]);
+    for (int r = k + 1; r < n; ++r) {
+      double v = std::fabs(a[(size_t)r * n + k]);
+      if (v > best) { best = v; pr = r; }
+    }
+    if (best == 0.0) return false;
+    piv[k] = pr;
+    if (pr != k)
+      for (int c = 0; c < n; ++c) std::swap(a[(size_t)k * n + c], a[(size_t)pr * n + c]);
+    double d = a[(size_t)k * n + k];
+    for (int r = k + 1; r < n; ++r) {
+      double l = a[(size_t)r * n + k] / d;
+      a[(size_t)r * n + k] = l;
+      for (int c = k + 1; c < n; ++c) a[(size_t)r * n + c] -= l * a[(size_t)k * n + c];
+    }
+  }
+  return true;
+}
+void lu_solve(const std::vector<double>& a, const std::vector<int>& piv, int n, double* x) {
+  for (int k = 0; k < n; ++k) std::swap(x[k], x[piv[k]]);
+  for (int r = 0; r < n; ++r) {
+    double s = x[r];
+    for (int c = 0; c < r; ++c) s -= a[(size_t)r * n + c] * x[c];
+    x[r] = s;
+  }
+  for (int r = n - 1; r >= 0; --r) {
+    double s = x[r];
+    for (int c = r + 1; c < n; ++c) s -= a[(size_t)r * n + c] * x[c];
+    x[r] = s / a[(size_t)r * n + r];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Element-by-element assembly of A = [[L, B^T],[B, 0]].
+//   L_ij = a(psi_j, psi_i) = nu int grad psi_j : grad psi_i
+//   B_kj = b(psi_j, phi_k) = - int phi_k div psi_j              (
+//          sign: reading 1 -- the standard sign that makes eq:stokes1 hold)
+// Triplets are generated in element order, then each row is stably sorted by
+// column and duplicates summed in element order.
+// --------------------------------------------------------------------------
+void assemble(Level& L, double nu) {
+  const int N = L.N;
+  const double h = L.h;
+  const int64_t nlat = L.nlat, nv = L.nv, npn = L.npn;
+  auto iux = [&](int64_t i, int64_t j) { return j * nlat + i; };
+  auto iuy = [&](int64_t i, int64_t j) { return nv + j * nlat + i; };
+  auto ipp = [&](int64_t kx, int64_t ky) { return 2 * nv + ky * npn + kx; };
+
+  // element matrices on the reference square mapped to [0,h]^2 (Jacobian h^2,
+  // d/dx = (1/h) d/dt); identical on every element of the uniform grid.
+  double Le[9][9] = {{0}}, Bxe[4][9] = {{0}}, Bye[4][9] = {{0}};
+  for (int qx = 0; qx < 3; ++qx)
+    for (int qy = 0; qy < 3; ++qy) {
+      double t = kGP[qx], s = kGP[qy], w = kGW[qx] * kGW[qy] * h * h;
+      double dx[9], dy[9];
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          dx[b * 3 + a] = dq2(a, t) * q2(b, s) / h;
+          dy[b * 3 + a] = q2(a, t) * dq2(b, s) / h;
+        }
+      for (int m = 0; m < 9; ++m)
+        for (int n2 = 0; n2 < 9; ++n2) Le[m][n2] += nu * w * (dx[m] * dx[n2] + dy[m] * dy[n2]);
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) {
+          double phi = q1(c, t) * q1(d, s);
+          for (int m = 0; m < 9; ++m) {
+            Bxe[d * 2 + c][m] += -w * phi * dx[m];
+            Bye[d * 2 + c][m] += -w * phi * dy[m];
+          }
+        }
+    }
+
+  const int64_t n = L.ntot;
+  std::vector<int64_t> cnt(n + 1, 0);
+  auto for_each_triplet = [&](auto&& emit) {
+    for (int ey = 0; ey < N; ++ey)
+      for (int ex = 0; ex < N; ++ex) {
+        int64_t vi[9], pi[4];
+        for (int b = 0; b < 3; ++b)
+          for (int a = 0; a < 3; ++a) vi[b * 3 + a] = iux(2 * ex + a, 2 * ey + b);
+        for (int d = 0; d < 2; ++d)
+          for (int c = 0; c < 2; ++c) pi[d * 2 + c] = ipp(ex + c, ey + d);
+        for (int m = 0; m < 9; ++m)
+          for (int n2 = 0; n2 < 9; ++n2) {
+            emit(vi[m], vi[n2], Le[m][n2]);            // L, x component
+            emit(vi[m] + nv, vi[n2] + nv, Le[m][n2]);  // L, y component
+          }
+        for (int k = 0; k < 4; ++k)
+          for (int m = 0; m < 9; ++m) {
+            emit(pi[k], vi[m], Bxe[k][m]);        // B_x
+            emit(pi[k], vi[m] + nv, Bye[k][m]);   // B_y
+            emit(vi[m], pi[k], Bxe[k][m]);        // B_x^T
+            emit(vi[m] + nv, pi[k], Bye[k][m]);   // B_y^T
+          }
+      }
+  };
+  for_each_triplet([&](int64_t r, int64_t, double) { cnt[r + 1]++; });
+  for (int64_t r = 0; r < n; ++r) cnt[r + 1] += cnt[r];
+  std::vector<int32_t> tc(cnt[n]);
+  std::vector<double> tv(cnt[n]);
+  {
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for_each_triplet([&](int64_t r, int64_t c, double v) {
+      int64_t q = pos[r]++;
+      tc[q] = (int32_t)c;
+      tv[q] = v;
+    });
+  }
+  // stable sort each row by column and sum duplicates (element order kept)
+  std::vector<int64_t> newcnt(n + 1, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t b = cnt[r], e = cnt[r + 1];
+    std::vector<int64_t> idx(e - b);
+    for (int64_t q = b; q < e; ++q) idx[q - b] = q;
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) { return tc[x] < tc[y]; });
+    std::vector<int32_t> c2;
+    std::vector<double> v2;
+    for (int64_t q : idx) {
+      if (!c2.empty() && c2.back() == tc[q]) v2.back() += tv[q];
+      else { c2.push_back(tc[q]); v2.push_back(tv[q]); }
+    }
+    for (size_t q = 0; q < c2.size(); ++q) { tc[b + q] = c2[q]; tv[b + q] = v2[q]; }
+    newcnt[r + 1] = (int64_t)c2.size();
+  }
+  for (int64_t r = 0; r < n; ++r) newcnt[r + 1] += newcnt[r];
+  L.A.nrows = n;
+  L.A.rowptr = newcnt;
+  L.A.col.resize(newcnt[n]);
+  L.A.val.resize(newcnt[n]);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t len = newcnt[r + 1] - newcnt[r];
+    std::memcpy(&L.A.col[newcnt[r]], &tc[cnt[r]], len * sizeof(int32_t));
+    std::memcpy(&L.A.val[newcnt[r]], &tv[cnt[r]], len * sizeof(double));
+  }
+
+  // Dirichlet velocity on all edges, both components (reading 2)
+  L.dir.assign(n, 0);
+  for (int64_t j = 0; j < nlat; ++j)
+    for (int64_t i = 0; i < nlat; ++i)
+      if (i == 0 || j == 0 || i == nlat - 1 || j == nlat - 1) {
+        L.dir[iux(i, j)] = 1;
+        L.dir[iuy(i, j)] = 1;
+      }
+}
+
+// y = A x, then Dirichlet rows set to 0 (the operator of the interior system)
+void matvec_masked(const Level& L, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < L.ntot; ++r) {
+    double s = 0;
+    for (int64_t q = L.A.rowptr[r]; q < L.A.rowptr[r + 1]; ++q) s += L.A.val[q] * x[L.A.col[q]];
+    y[r] = L.dir[r] ? 0.0 : s;
+  }
+}
+
+// r = b - A x on non-Dirichlet rows, 0 on Dirichlet rows (alg:mg line 3)
+void residual(const Level& L, const double* x, const double* b, double* r) {
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < L.ntot; ++q) {
+    double s = b[q];
+    for (int64_t k = L.A.rowptr[q]; k < L.A.rowptr[q + 1]; ++k) s -= L.A.val[k] * x[L.A.col[k]];
+    r[q] = L.dir[q] ? 0.0 : s;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Vanka patches.  Patch (kx,ky), 0<=kx,ky<=N, one per pressure node
+// (reading 7: boundary nodes included, as tab:rwf's 76+124l+51l^2 requires):
+// the pressure DOF at the node plus every velocity DOF (both components) of the
+// <=2x2 elements around it, i.e. lattice window [2kx-2,2kx+2]x[2ky-2,2ky+2]
+// clipped to the domain, minus Dirichlet DOFs (reading 7).
+// A_i = V_i A V_i^T is extracted from the globally assembled A (reading 8) and
+// LU-factored once ("inverting each patch matrix ahead of time");
+// bitwise-identical A_i share one factorisation (tuned Vanka).
+// --------------------------------------------------------------------------
+bool build_patches(Level& L, double omega, int weighting, std::string& err) {
+  const int N = L.N;
+  const int64_t nlat = L.nlat, nv = L.nv, npn = L.npn;
+  const int64_t npatch = (int64_t)(N + 1) * (N + 1);
+  L.pstart.assign(npatch + 1, 0);
+  L.pdof.clear();
+  for (int ky = 0; ky <= N; ++ky)
+    for (int kx = 0; kx <= N; ++kx) {
+      for (int comp = 0; comp < 2; ++comp)
+        for (int64_t j = 2 * ky - 2; j <= 2 * ky + 2; ++j)
+          for (int64_t i = 2 * kx - 2; i <= 2 * kx + 2; ++i) {
+            if (i < 0 || j < 0 || i >= nlat || j >= nlat) continue;
+            int64_t g = comp * nv + j * nlat + i;
+            if (!L.dir[g]) L.pdof.push_back(g);
+          }
+      L.pdof.push_back(2 * nv + (int64_t)ky * npn + kx);
+      L.pstart[(int64_t)ky * (N + 1) + kx + 1] = (int64_t)L.pdof.size();
+    }
+  // extract every A_i, deduplicate by bitwise equality
+  std::map<std::string, int> seen;
+  L.pgroup.assign(npatch, -1);
+  L.glu.clear();
+  L.gpiv.clear();
+  L.gsize.clear();
+  std::vector<std::string> keys(npatch);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t p = 0; p < npatch; ++p) {
+    int64_t b = L.pstart[p], e = L.pstart[p + 1];
+    int n = (int)(e - b);
+    std::vector<double> Ai((size_t)n * n, 0.0);
+    for (int r = 0; r < n; ++r) {
+      int64_t g = L.pdof[b + r];
+      for (int64_t q = L.A.rowptr[g]; q < L.A.rowptr[g + 1]; ++q) {
+        int64_t c = L.A.col[q];
+        for (int cc = 0; cc < n; ++cc)
+          if (L.pdof[b + cc] == c) { Ai[(size_t)r * n + cc] = L.A.val[q]; break; }
+      }
+    }
+    std::string key((const char*)&n, sizeof(int));
+    key.append((const char*)Ai.data(), Ai.size() * sizeof(double));
+    keys[p] = std::move(key);
+  }
+  for (int64_t p = 0; p < npatch; ++p) {
+    auto it = seen.find(keys[p]);
+    if (it != seen.end()) { L.pgroup[p] = it->second; continue; }
+    int n;
+    std::memcpy(&n, keys[p].data(), sizeof(int));
+    std::vector<double> Ai((size_t)n * n);
+    std::memcpy(Ai.data(), keys[p].data() + sizeof(int), Ai.size() * sizeof(double));
+    std::vector<int> piv;
+    if (!lu_factor(Ai, piv, n)) { err = "singular patch matrix"; return false; }
+    int gid = (int)L.glu.size();
+    L.glu.push_back(std::move(Ai));
+    L.gpiv.push_back(std::move(piv));
+    L.gsize.push_back(n);
+    seen.emplace(keys[p], gid);
+    L.pgroup[p] = gid;
+  }
+  // weights W_i ("the matrix with the weights"; reading 6):
+  // multiplicity weighting omega/mult(j), mult(j) = number of patches holding j
+  std::vector<int> mult(L.ntot, 0);
+  for (int64_t q = 0; q < (int64_t)L.pdof.size(); ++q) mult[L.pdof[q]]++;
+  L.weight.assign(L.ntot, 0.0);
+  for (int64_t g = 0; g < L.ntot; ++g)
+    if (mult[g] > 0) L.weight[g] = weighting == 0 ? omega / mult[g] : omega;
+  return true;
+}
+
+// x_out = x_in + sum_i V_i^T W_i A_i^{-1} V_i (b - A x_in)   (alg:vk)
+// patch solves in parallel, accumulation serial in ascending patch order
+void vanka_sweep(const Level& L, const double* xin, const double* b, double* xout) {
+  const int64_t npatch = (int64_t)L.pstart.size() - 1;
+  std::vector<double> r(L.ntot);
+  residual(L, xin, b, r.data());
+  std::vector<double> delta(L.pdof.size());
+#pragma omp parallel for schedule(static)
+  for (int64_t p = 0; p < npatch; ++p) {
+    int64_t s = L.pstart[p];
+    int n = (int)(L.pstart[p + 1] - s);
+    double* d = &delta[s];
+    for (int q = 0; q < n; ++q) d[q] = r[L.pdof[s + q]];  // V_i r
+    int g = L.pgroup[p];
+    lu_solve(L.glu[g], L.gpiv[g], n, d);                   // A_i^{-1} V_i r
+  }
+  std::vector<double> acc(L.ntot, 0.0);
+  for (int64_t q = 0; q < (int64_t)L.pdof.size(); ++q) {
+    int64_t g = L.pdof[q];
+    acc[g] += L.weight[g] * delta[q];
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < L.ntot; ++q) xout[q] = xin[q] + acc[q];
+}
+
+// --------------------------------------------------------------------------
+// Interpolation P_{l-1}: coarse -> fine, the finite-element interpolation of the
+// nested Q2 / Q1 spaces: row of a fine DOF = coarse basis functions
+// evaluated at the fine DOF's coordinates.
+// --------------------------------------------------------------------------
+void build_prolongation(const Level& C, Level& F) {
+  const int64_t fl = F.nlat, cl = C.nlat;
+  std::vector<std::vector<std::pair<int32_t, double>>> rows(F.ntot);
+  for (int comp = 0; comp < 2; ++comp)
+    for (int64_t j = 0; j < fl; ++j)
+      for (int64_t i = 0; i < fl; ++i) {
+        // fine lattice i sits at i*hf/2 = (i/4)*hc: coarse element floor(i/4)
+        int64_t ex = std::min<int64_t>(i / 4, C.N - 1), ey = std::min<int64_t>(j / 4, C.N - 1);
+        double t = (i - 4.0 * ex) / 4.0, s = (j - 4.0 * ey) / 4.0;
+        auto& row = rows[comp * F.nv + j * fl + i];
+        for (int b = 0; b < 3; ++b)
+          for (int a = 0; a < 3; ++a) {
+            double w = q2(a, t) * q2(b, s);
+            if (w != 0.0) row.push_back({(int32_t)(comp * C.nv + (2 * ey + b) * cl + 2 * ex + a), w});
+          }
+      }
+  for (int64_t ky = 0; ky < F.npn; ++ky)
+    for (int64_t kx = 0; kx < F.npn; ++kx) {
+      int64_t ex = std::min<int64_t>(kx / 2, C.N - 1), ey = std::min<int64_t>(ky / 2, C.N - 1);
+      double t = (kx - 2.0 * ex) / 2.0, s = (ky - 2.0 * ey) / 2.0;
+      auto& row = rows[2 * F.nv + ky * F.npn + kx];
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) {
+          double w = q1(c, t) * q1(d, s);
+          if (w != 0.0) row.push_back({(int32_t)(2 * C.nv + (ey + d) * C.npn + ex + c), w});
+        }
+    }
+  F.P.nrows = F.ntot;
+  F.P.rowptr.assign(F.ntot + 1, 0);
+  for (int64_t r = 0; r < F.ntot; ++r) F.P.rowptr[r + 1] = F.P.rowptr[r] + (int64_t)rows[r].size();
+  F.P.col.resize(F.P.rowptr[F.ntot]);
+  F.P.val.resize(F.P.rowptr[F.ntot]);
+  for (int64_t r = 0; r < F.ntot; ++r)
+    for (size_t q = 0; q < rows[r].size(); ++q) {
+      F.P.col[F.P.rowptr[r] + q] = rows[r][q].first;
+      F.P.val[F.P.rowptr[r] + q] = rows[r][q].second;
+    }
+  // explicit transpose (restriction = P^T)
+  Csr& T = F.PT;
+  T.nrows = C.ntot;
+  T.rowptr.assign(C.ntot + 1, 0);
+  for (int64_t q = 0; q < (int64_t)F.P.col.size(); ++q) T.rowptr[F.P.col[q] + 1]++;
+  for (int64_t r = 0; r < C.ntot; ++r) T.rowptr[r + 1] += T.rowptr[r];
+  T.col.resize(F.P.col.size());
+  T.val.resize(F.P.col.size());
+  std::vector<int64_t> pos(T.rowptr.begin(), T.rowptr.end() - 1);
+  for (int64_t r = 0; r < F.ntot; ++r)
+    for (int64_t q = F.P.rowptr[r]; q < F.P.rowptr[r + 1]; ++q) {
+      int64_t c = F.P.col[q];
+      T.col[pos[c]] = (int32_t)r;
+      T.val[pos[c]] = F.P.val[q];
+      pos[c]++;
+    }
+}
+
+// r_c = P^T r_f with coarse Dirichlet rows set to 0 (alg:mg line 4; reading 9)
+void restrict_(const Level& C, const Level& F, const double* rf, double* rc) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < C.ntot; ++r) {
+    double s = 0;
+    for (int64_t q = F.PT.rowptr[r]; q < F.PT.rowptr[r + 1]; ++q) s += F.PT.val[q] * rf[F.PT.col[q]];
+    rc[r] = C.dir[r] ? 0.0 : s;
+  }
+}
+// x_f += P e_c  (alg:mg line 9)
+void prolong_add(const Level& F, const double* ec, double* xf) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < F.ntot; ++r) {
+    double s = 0;
+    for (int64_t q = F.P.rowptr[r]; q < F.P.rowptr[r + 1]; ++q) s += F.P.val[q] * ec[F.P.col[q]];
+    xf[r] += s;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Level-0 solve "A_0^{-1}".  A_0 restricted to the non-Dirichlet
+// DOFs is singular with the constant pressure as its null vector (P:66,
+// reading 3); we take the minimum-norm solution via the bordered system
+//   [[A_II, n],[n^T, 0]] [x; lambda] = [b_I; 0],   n = 1_p / sqrt(m),
+// whose x equals pinv(A_II) b_I for any b_I (tests pin this to numpy.pinv).
+// --------------------------------------------------------------------------
+bool build_coarse(Level& L, std::string& err) {
+  L.interior.clear();
+  for (int64_t g = 0; g < L.ntot; ++g)
+    if (!L.dir[g]) L.interior.push_back(g);
+  const int ni = (int)L.interior.size();
+  const int n = ni + 1;
+  std::vector<int64_t> loc(L.ntot, -1);
+  for (int q = 0; q < ni; ++q) loc[L.interior[q]] = q;
+  std::vector<double> M((size_t)n * n, 0.0);
+  for (int r = 0; r < ni; ++r) {
+    int64_t g = L.interior[r];
+    for (int64_t q = L.A.rowptr[g]; q < L.A.rowptr[g + 1]; ++q) {
+      int64_t c = loc[L.A.col[q]];
+      if (c >= 0) M[(size_t)r * n + c] = L.A.val[q];
+    }
+  }
+  const double nv = 1.0 / std::sqrt((double)L.np);
+  for (int r = 0; r < ni; ++r)
+    if (L.interior[r] >= 2 * L.nv) {
+      M[(size_t)r * n + ni] = nv;
+      M[(size_t)ni * n + r] = nv;
+    }
+  if (!lu_factor(M, L.cpiv, n)) { err = "singular coarse matrix"; return false; }
+  L.clu = std::move(M);
+  L.cn = n;
+  return true;
+}
+void coarse_solve(const Level& L, const double* b, double* x) {
+  std::vector<double> rhs(L.cn, 0.0);
+  const int ni = L.cn - 1;
+  for (int q = 0; q < ni; ++q) rhs[q] = b[L.interior[q]];
+  lu_solve(L.clu, L.cpiv, L.cn, rhs.data());
+  std::fill(x, x + L.ntot, 0.0);
+  for (int q = 0; q < ni; ++q) x[L.interior[q]] = rhs[q];
+}
+
+// --------------------------------------------------------------------------
+// V-cycle, alg:mg, V(nu1, nu2); x is in/out on level l.
+// --------------------------------------------------------------------------
+void mg(const Ctx& c, int l, const double* b, double* x) {
+  const Level& L = c.lev[l];
+  if (l == 0) {  // only reached when the hierarchy has a single level
+    if (c.coarse_mode == 0) coarse_solve(L, b, x);
+    else {
+      std::vector<double> t(L.ntot);
+      for (int s = 0; s < 3; ++s) { vanka_sweep(L, x, b, t.data()); std::copy(t.begin(), t.end(), x); }
+    }
+    return;
+  }
+  std::vector<double> t(L.ntot), r(L.ntot);
+  for (int s = 0; s < c.nu1; ++s) {  // "Relax on u_l and p_l"
+    vanka_sweep(L, x, b, t.data());
+    std::copy(t.begin(), t.end(), x);
+  }
+  residual(L, x, b, r.data());  // "Compute residual"
+  const Level& C = c.lev[l - 1];
+  std::vector<double> rc(C.ntot), ec(C.ntot, 0.0);
+  restrict_(C, L, r.data(), rc.data());  // "Restriction"
+  if (l == 1) {
+    if (c.coarse_mode == 0) coarse_solve(C, rc.data(), ec.data());  // "e_0 = A_0^{-1} r_0"
+    else {
+      std::vector<double> t0(C.ntot);
+      for (int s = 0; s < 3; ++s) { vanka_sweep(C, ec.data(), rc.data(), t0.data()); ec = t0; }
+    }
+  } else {
+    mg(c, l - 1, rc.data(), ec.data());  // "MG(A_{l-1}, 0, 0, r_{u,l-1}, r_{p,l-1}, l-1)"
+  }
+  prolong_add(L, ec.data(), x);  // "Correction"
+  for (int s = 0; s < c.nu2; ++s) {  // "Relax on u_l and p_l"
+    vanka_sweep(L, x, b, t.data());
+    std::copy(t.begin(), t.end(), x);
+  }
+}
+
+// deterministic blocked dot product (fixed 4096-element blocks)
+double dot(const double* a, const double* b, int64_t n) {
+  const int64_t B = 4096;
+  int64_t nb = (n + B - 1) / B;
+  std::vector<double> part(nb, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nb; ++k) {
+    double s = 0;
+    for (int64_t q = k * B; q < std::min(n, (k + 1) * B); ++q) s += a[q] * b[q];
+    part[k] = s;
+  }
+  double s = 0;
+  for (double v : part) s += v;
+  return s;
+}
+
+}  // namespace
+
+// =============================================================================
+// extern "C" surface used by oracle/__init__.py (ctypes)
+// =============================================================================
+extern "C" {
+
+void* orc_create(int n_elem, int n_coarse, double nu, double omega, int weighting, int nu1, int nu2,
+                 int coarse_mode) {
+  if (n_elem < 1 || n_coarse < 1 || n_elem < n_coarse) return nullptr;
+  int nl = 1;
+  for (int n = n_elem; n > n_coarse; n /= 2) {
+    if (n % 2) return nullptr;
+    nl++;
+  }
+  if ((n_elem >> (nl - 1)) != n_coarse) return nullptr;
+  Ctx* c = new Ctx;
+  c->nu = nu;
+  c->omega = omega;
+  c->weighting = weighting;
+  c->nu1 = nu1;
+  c->nu2 = nu2;
+  c->coarse_mode = coarse_mode;
+  c->lev.resize(nl);
+  for (int l = 0; l < nl; ++l) {
+    Level& L = c->lev[l];
+    L.N = n_coarse << l;
+    L.h = 1.0 / L.N;
+    L.nlat = 2 * L.N + 1;
+    L.nv = L.nlat * L.nlat;
+    L.npn = L.N + 1;
+    L.np = L.npn * L.npn;
+    L.ntot = 2 * L.nv + L.np;
+    assemble(L, nu);
+    if (!build_patches(L, omega, weighting, c->err)) { delete c; return nullptr; }
+    if (l > 0) build_prolongation(c->lev[l - 1], L);
+  }
+  if (!build_coarse(c->lev[0], c->err)) { delete c; return nullptr; }
+  return c;
+}
+void orc_destroy(void* h) { delete (Ctx*)h; }
+int orc_num_levels(void* h) { return (int)((Ctx*)h)->lev.size(); }
+int64_t orc_level_len(void* h, int l) { return ((Ctx*)h)->lev[l].ntot; }
+int orc_level_n(void* h, int l) { return ((Ctx*)h)->lev[l].N; }
+int orc_num_groups(void* h, int l) { return (int)((Ctx*)h)->lev[l].glu.size(); }
+int64_t orc_nnz(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].A.col.size(); }
+int orc_max_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+// export the full assembled CSR (before Dirichlet masking)
+void orc_csr(void* h, int l, int64_t* rowptr, int32_t* col, double* val) {
+  const Csr& A = ((Ctx*)h)->lev[l].A;
+  std::memcpy(rowptr, A.rowptr.data(), A.rowptr.size() * sizeof(int64_t));
+  std::memcpy(col, A.col.data(), A.col.size() * sizeof(int32_t));
+  std::memcpy(val, A.val.data(), A.val.size() * sizeof(double));
+}
+void orc_dirichlet(void* h, int l, uint8_t* out) {
+  const Level& L = ((Ctx*)h)->lev[l];
+  std::memcpy(out, L.dir.data(), L.ntot);
+}
+void orc_weights(void* h, int l, double* out) {
+  const Level& L = ((Ctx*)h)->lev[l];
+  std::memcpy(out, L.weight.data(), L.ntot * sizeof(double));
+}
+// patch (kx,ky): n dofs (<=51), global dof list, group id
+int orc_patch(void* h, int l, int kx, int ky, int64_t* dofs) {
+  const Level& L = ((Ctx*)h)->lev[l];
+  int64_t p = (int64_t)ky * (L.N + 1) + kx;
+  int64_t s = L.pstart[p], e = L.pstart[p + 1];
+  for (int64_t q = s; q < e; ++q) dofs[q - s] = L.pdof[q];
+  return (int)(e - s);
+}
+int orc_patch_group(void* h, int l, int kx, int ky) {
+  const Level& L = ((Ctx*)h)->lev[l];
+  return L.pgroup[(int64_t)ky * (L.N + 1) + kx];
+}
+int64_t orc_total_patch_dofs(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].pdof.size(); }
+
+// problem data on level l (kind: 0 ZERO, 1 MMS_PAPER, 2 MMS_INSPACE, 3 CAVITY)
+// b: velocity = (f, psi_i) by quadrature (boundary rows hold the boundary value,
+//    they are masked anyway), pressure = 0 (eq:stokesmatrix right side [f; 0]).
+// x0: boundary velocity values, zero elsewhere (reading 10).
+void orc_problem(void* h, int l, int kind, double* b, double* x0) {
+  const Ctx& c = *(Ctx*)h;
+  const Level& L = c.lev[l];
+  const int N = L.N;
+  const double hh = L.h;
+  std::fill(b, b + L.ntot, 0.0);
+  std::fill(x0, x0 + L.ntot, 0.0);
+  for (int ey = 0; ey < N; ++ey)
+    for (int ex = 0; ex < N; ++ex)
+      for (int qx = 0; qx < 3; ++qx)
+        for (int qy = 0; qy < 3; ++qy) {
+          double t = kGP[qx], s = kGP[qy], w = kGW[qx] * kGW[qy] * hh * hh;
+          double x = (ex + t) * hh, y = (ey + s) * hh, fx, fy;
+          forcing(kind, c.nu, x, y, &fx, &fy);
+          for (int bb = 0; bb < 3; ++bb)
+            for (int a = 0; a < 3; ++a) {
+              double psi = q2(a, t) * q2(bb, s);
+              int64_t g = (int64_t)(2 * ey + bb) * L.nlat + 2 * ex + a;
+              b[g] += w * fx * psi;
+              b[L.nv + g] += w * fy * psi;
+            }
+        }
+  for (int64_t j = 0; j < L.nlat; ++j)
+    for (int64_t i = 0; i < L.nlat; ++i) {
+      int64_t g = j * L.nlat + i;
+      if (!L.dir[g]) continue;
+      double x = i * hh / 2, y = j * hh / 2, ux, uy;
+      if (kind == 3) {  // lid-driven cavity (reading 15): u = (1,0) on the lid, 0 < x < 1
+        ux = (j == L.nlat - 1 && i > 0 && i < L.nlat - 1) ? 1.0 : 0.0;
+        uy = 0.0;
+      } else {
+        exact_u(kind, x, y, &ux, &uy);
+      }
+      x0[g] = ux;
+      x0[L.nv + g] = uy;
+      b[g] = ux;
+      b[L.nv + g] = uy;
+    }
+}
+// exact nodal values of the manufactured solution (for the exactness pins)
+void orc_exact(void* h, int l, int kind, double* out) {
+  const Level& L = ((Ctx*)h)->lev[l];
+  for (int64_t j = 0; j < L.nlat; ++j)
+    for (int64_t i = 0; i < L.nlat; ++i) {
+      double ux, uy;
+      exact_u(kind, i * L.h / 2, j * L.h / 2, &ux, &uy);
+      out[j * L.nlat + i] = ux;
+      out[L.nv + j * L.nlat + i] = uy;
+    }
+  for (int64_t ky = 0; ky < L.npn; ++ky)
+    for (int64_t kx = 0; kx < L.npn; ++kx) exact_p(kind, kx * L.h, ky * L.h, &out[2 * L.nv + ky * L.npn + kx]);
+}
+
+void orc_matvec(void* h, int l, const double* x, double* y) { matvec_masked(((Ctx*)h)->lev[l], x, y); }
+void orc_residual(void* h, int l, const double* x, const double* b, double* r) {
+  residual(((Ctx*)h)->lev[l], x, b, r);
+}
+void orc_vanka_sweep(void* h, int l, const double* xin, const double* b, double* xout) {
+  vanka_sweep(((Ctx*)h)->lev[l], xin, b, xout);
+}
+// level l is the FINE level (l >= 1)
+void orc_restrict(void* h, int l, const double* rf, double* rc) {
+  const Ctx& c = *(Ctx*)h;
+  restrict_(c.lev[l - 1], c.lev[l], rf, rc);
+}
+void orc_prolong_add(void* h, int l, const double* ec, double* xf) { prolong_add(((Ctx*)h)->lev[l], ec, xf); }
+void orc_prolongation_csr(void* h, int l, int64_t* rowptr, int32_t* col, double* val) {
+  const Csr& P = ((Ctx*)h)->lev[l].P;
+  std::memcpy(rowptr, P.rowptr.data(), P.rowptr.size() * sizeof(int64_t));
+  std::memcpy(col, P.col.data(), P.col.size() * sizeof(int32_t));
+  std::memcpy(val, P.val.data(), P.val.size() * sizeof(double));
+}
+int64_t orc_prolongation_nnz(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].P.col.size(); }
+void orc_coarse_solve(void* h, const double* b, double* x) { coarse_solve(((Ctx*)h)->lev[0], b, x); }
+// one V-cycle on the finest level: x in/out
+void orc_vcycle(void* h, const double* b, double* x) {
+  const Ctx& c = *(Ctx*)h;
+  mg(c, (int)c.lev.size() - 1, b, x);
+}
+
+// Right-preconditioned flexible GMRES: Arnoldi with modified
+// Gram-Schmidt, Givens rotations, no restart; the preconditioner is one V-cycle
+// started from zero.  x is in (x0) / out.  hist[0..its] = |g_{k}|/beta (the
+// GMRES residual estimate, = the true relative residual in exact arithmetic).
+// returns iterations; *true_rel = ||b - A x|| / ||b - A x0|| recomputed.
+// status: 0 converged, 1 not converged, 2 non-finite.
+int orc_fgmres(void* h, const double* b, double* x, double rtol, int maxit, double* hist, double* true_rel,
+               int* status) {
+  const Ctx& c = *(Ctx*)h;
+  const Level& L = c.lev.back();
+  const int64_t n = L.ntot;
+  std::vector<double> r(n);
+  residual(L, x, b, r.data());
+  double beta = std::sqrt(dot(r.data(), r.data(), n));
+  hist[0] = 1.0;
+  *status = 0;
+  *true_rel = 0.0;
+  if (beta == 0.0) return 0;
+  std::vector<std::vector<double>> V, Z;
+  V.emplace_back(n);
+  for (int64_t q = 0; q < n; ++q) V[0][q] = r[q] / beta;
+  std::vector<std::vector<double>> H(maxit + 1, std::vector<double>(maxit, 0.0));
+  std::vector<double> cs(maxit), sn(maxit), g(maxit + 1, 0.0);
+  g[0] = beta;
+  int k = 0;
+  bool conv = false;
+  for (int j = 0; j < maxit; ++j) {
+    Z.emplace_back(n, 0.0);
+    mg(c, (int)c.lev.size() - 1, V[j].data(), Z[j].data());  // z_j = M v_j
+    std::vector<double> w(n);
+    matvec_masked(L, Z[j].data(), w.data());                  // w = A z_j
+    for (int i = 0; i <= j; ++i) {                            // modified Gram-Schmidt
+      H[i][j] = dot(w.data(), V[i].data(), n);
+      for (int64_t q = 0; q < n; ++q) w[q] -= H[i][j] * V[i][q];
+    }
+    H[j + 1][j] = std::sqrt(dot(w.data(), w.data(), n));
+    if (!std::isfinite(H[j + 1][j])) { *status = 2; return j; }
+    for (int i = 0; i < j; ++i) {  // previous rotations
+      double t = cs[i] * H[i][j] + sn[i] * H[i + 1][j];
+      H[i + 1][j] = -sn[i] * H[i][j] + cs[i] * H[i + 1][j];
+      H[i][j] = t;
+    }
+    double a = H[j][j], bb = H[j + 1][j], rr = std::hypot(a, bb);
+    cs[j] = a / rr;
+    sn[j] = bb / rr;
+    H[j][j] = rr;
+    H[j + 1][j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    hist[j + 1] = std::fabs(g[j + 1]) / beta;
+    k = j + 1;
+    double hn = bb;
+    if (hist[j + 1] <= rtol || hn == 0.0) { conv = true; break; }
+    V.emplace_back(n);
+    for (int64_t q = 0; q < n; ++q) V[j + 1][q] = w[q] / hn;
+  }
+  // y = R^{-1} g ; x = x0 + Z y
+  std::vector<double> y(k);
+  for (int i = k - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int m = i + 1; m < k; ++m) s -= H[i][m] * y[m];
+    y[i] = s / H[i][i];
+  }
+  for (int i = 0; i < k; ++i)
+    for (int64_t q = 0; q < n; ++q) x[q] += y[i] * Z[i][q];
+  residual(L, x, b, r.data());
+  *true_rel = std::sqrt(dot(r.data(), r.data(), n)) / beta;
+  if (!std::isfinite(*true_rel)) *status = 2;
+  else if (!conv) *status = 1;
+  return k;
+}
+
+}  // extern "C"
