@@ -1,0 +1,217 @@
+/*
+ * svk.h -- C ABI of libsvk: B200-native (sm_100a, fp64) additive-Vanka
+ * monolithic multigrid for Q2-Q1 Taylor-Hood Stokes, after Spies, Olson,
+ * MacLachlan, "Exploiting mesh structure to improve multigrid performance for
+ * saddle point problems" (arXiv 2401.06277).
+ *
+ * Citations: P:n = line n of the paper's text, with its label.
+ *
+ * Problem: -nu Lap u + grad p = f, div u = 0 on [0,1]^2, Q2-Q1
+ * Taylor-Hood on a uniform N x N grid, A = [[L, B^T],[B, 0]]
+ * (eq:stokesmatrix), velocity Dirichlet on every edge.  The library solves the
+ * interior system: Dirichlet entries of a vector hold boundary data and are
+ * never changed by a correction; every residual is 0 on Dirichlet rows.
+ *
+ * ---------------------------------------------------------------------------
+ * VECTORS.  Every vector argument is a caller-owned DEVICE buffer of double
+ * (8-byte aligned; 256-byte aligned recommended) holding one level's vector
+ * in the PITCHED layout reported by svk_level_info():
+ *   u_x plane at off_ux: (2N+1) rows (y) of pitch_u doubles, column i = x index
+ *   u_y plane at off_uy: same shape
+ *   p   plane at off_p : (N+1) rows of pitch_p doubles
+ * Lattice point (i,j), 0<=i,j<=2N, is at (i h/2, j h/2), h = 1/N; pressure
+ * node (kx,ky) at (kx h, ky h).  Padding columns (i > 2N, kx > N) and the gaps
+ * between planes must be 0 on input; the library keeps them 0 in outputs.
+ * Length vec_len doubles.  Levels: 0 = coarsest (N0), L-1 = finest (P:146,
+ * alg:mg "level 0 is the coarsest grid").
+ *
+ * OWNERSHIP.  The library never frees or retains caller pointers beyond the
+ * stream-ordered completion of the call.  It owns its workspaces (patch
+ * inverses, per-level temporaries, Krylov basis), allocated with cudaMalloc
+ * on cfg.device in svk_create / on first use, and freed in svk_destroy.
+ *
+ * STREAMS.  `stream` is a cudaStream_t (NULL = legacy default stream).  Every
+ * call is asynchronous on `stream` except svk_create, svk_destroy,
+ * svk_fgmres / svk_solve_host (synchronise once per Krylov iteration for the
+ * Givens update and return on completion) and the introspection calls.
+ *
+ * ERRORS.  int status: SVK_OK = 0; negative = error (message via
+ * svk_last_error); SVK_NOT_CONVERGED = 1 is non-fatal (the report is filled).
+ * SVK_ERR_INVALID: bad level / size / NULL or misaligned pointer;
+ * SVK_ERR_CUDA: a CUDA runtime error (the context may be unusable afterwards);
+ * SVK_ERR_SINGULAR: a patch or coarse factorisation met a zero pivot;
+ * SVK_ERR_NONFINITE: FGMRES met NaN/Inf.
+ *
+ * THREADING.  One context per device; calls on one context must not overlap
+ * (scratch is per context).  Different contexts are independent.
+ */
+#ifndef SVK_H_
+#define SVK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVK_VERSION 1
+
+enum svk_status {
+  SVK_OK = 0,
+  SVK_NOT_CONVERGED = 1,
+  SVK_ERR_INVALID = -1,
+  SVK_ERR_CUDA = -2,
+  SVK_ERR_NCCL = -3,
+  SVK_ERR_SINGULAR = -4,
+  SVK_ERR_NONFINITE = -5,
+  SVK_ERR_ALLOC = -6
+};
+
+/* W_i of alg:vk ("the matrix with the weights"; unstated in the paper):
+ * MULT: omega_v / (number of patches holding the DOF) -- default (reading 6);
+ * SCALAR: omega_v * I. */
+enum svk_weighting { SVK_WEIGHT_MULT = 0, SVK_WEIGHT_SCALAR = 1 };
+
+/* level-0 solve ("an exact solve ... or three sweeps of the relaxation"):
+ * EXACT = minimum-norm solve (pressure mean 0; reading 3), SWEEPS3. */
+enum svk_coarse { SVK_COARSE_EXACT = 0, SVK_COARSE_SWEEPS3 = 1 };
+
+/* problem kinds for svk_set_problem:
+ * ZERO: b = 0, x0 = 0;
+ * MMS_PAPER: the paper's manufactured solution, f = -nu Lap u + grad p;
+ * MMS_INSPACE: u = (2x^2y, -2xy^2), p = xy - 1/4 (lies in the Q2-Q1 space);
+ * CAVITY: f = 0, u = (1,0) on lattice points of the lid y=1 with 0<x<1
+ *         (not in the paper; reading 15). */
+enum svk_problem { SVK_PROBLEM_ZERO = 0, SVK_PROBLEM_MMS_PAPER = 1, SVK_PROBLEM_MMS_INSPACE = 2, SVK_PROBLEM_CAVITY = 3 };
+
+/* sweep kernel selection (all compute alg:vk exactly; they differ in data flow):
+ * FUSED  (default) -- residual + patch solve + owner-computes gather in one kernel;
+ * UNFUSED -- residual, per-patch solve into a packed buffer, gather update
+ *            (the paper's form/apply/update kernel split), kept as a
+ *            cross-check of the fused kernel. */
+enum svk_sweep_impl { SVK_SWEEP_FUSED = 0, SVK_SWEEP_UNFUSED = 1 };
+
+typedef struct svk_config {
+  int32_t n_elem;     /* N, elements per side of the finest grid; N = n_coarse * 2^k */
+  int32_t n_coarse;   /* N0 >= 4 (all 25 patch categories exist; reading 4); default 4 */
+  double nu;          /* viscosity; default 1 */
+  double omega_v;     /* Vanka damping (reading 6); default 0.8 */
+  int32_t weighting;  /* enum svk_weighting; default MULT */
+  int32_t nu_pre;     /* pre-smoothing sweeps (V(1,1)); default 1 */
+  int32_t nu_post;    /* post-smoothing sweeps; default 1 */
+  int32_t coarse;     /* enum svk_coarse; default EXACT */
+  int32_t sweep_impl; /* enum svk_sweep_impl; default FUSED */
+  int32_t device;     /* CUDA device ordinal; default 0 */
+  int32_t reserved[8];
+} svk_config;
+
+typedef struct svk_level {
+  int32_t N;          /* elements per side on this level */
+  int32_t lat;        /* 2N+1 velocity lattice points per side */
+  int64_t vec_len;    /* doubles per vector */
+  int64_t off_ux, off_uy, off_p;  /* plane offsets (doubles) */
+  int64_t pitch_u, pitch_p;       /* row pitches (doubles), multiples of 8 */
+  int64_t n_dof;      /* 2(2N+1)^2 + (N+1)^2 (Dirichlet DOFs included) */
+  int64_t n_patch;    /* (N+1)^2 Vanka patches, one per pressure node */
+} svk_level;
+
+typedef struct svk_report {
+  int32_t iterations;      /* FGMRES iterations (= preconditioner applications) */
+  int32_t converged;       /* 1 if estimate <= rtol */
+  int32_t status;          /* same as the return value */
+  int32_t reserved;
+  double rel_residual;     /* true ||b - A x|| / ||b - A x0||, recomputed at exit */
+  double t_total_s;        /* wall time of the call (host clock) */
+  double t_vcycle_s;       /* device time in V-cycles (CUDA events) */
+  double t_orth_s;         /* device time in matvec + orthogonalisation */
+} svk_report;
+
+typedef struct svk_ctx svk_ctx;
+
+/* Fill *cfg with the defaults above for a grid of n_elem elements per side. */
+int svk_config_default(svk_config* cfg, int32_t n_elem);
+
+/* Grid create + hierarchy build and batched patch setup
+ * (a2): builds levels N, N/2, ..., N0, uploads the stencil tables, runs the
+ * patch-setup kernel that assembles and inverts the 25 distinct patch matrices
+ * of every level in fp64 ("inverting each patch matrix ahead of time", P:260;
+ * "25 different patch matrices"), and the minimum-norm level-0
+ * pseudo-inverse.  Synchronous.  On error *out = NULL. */
+int svk_create(const svk_config* cfg, svk_ctx** out);
+int svk_destroy(svk_ctx* ctx);
+
+int svk_num_levels(const svk_ctx* ctx, int32_t* levels);
+int svk_level_info(const svk_ctx* ctx, int32_t level, svk_level* out);
+
+/* Problem data on `level`: b (velocity: (f, psi_i) by 3x3 Gauss per element;
+ * Dirichlet rows: the boundary value; pressure: 0) and x0 (boundary values,
+ * zero elsewhere).  Either pointer may be NULL. */
+int svk_set_problem(svk_ctx* ctx, int32_t level, int32_t kind, double* b, double* x0, void* stream);
+
+/* r = b - A x on non-Dirichlet rows, 0 on Dirichlet rows (alg:mg line 3, P:151;
+ * kernels "Q2 matrix * Q2 vector", "Q2Q1 matrix * Q2/Q1 vector").
+ * r must not alias x or b. */
+int svk_residual(svk_ctx* ctx, int32_t level, const double* x, const double* b, double* r, void* stream);
+
+/* y = A x on non-Dirichlet rows, 0 on Dirichlet rows (the interior operator
+ * FGMRES iterates with).  y must not alias x. */
+int svk_matvec(svk_ctx* ctx, int32_t level, const double* x, double* y, void* stream);
+
+/* nsweeps additive Vanka sweeps (alg:vk):
+ *   x <- x + sum_i V_i^T W_i A_i^{-1} V_i (b - A x)
+ * with one patch per pressure node and exact patch solves.  Out of place:
+ * reads x_in, writes x_out (x_out must not alias x_in or b); for nsweeps > 1
+ * the library ping-pongs through its own workspace and the final iterate is
+ * in x_out. */
+int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out,
+                    int32_t nsweeps, void* stream);
+
+/* r_coarse = P^T r_fine on level-1 with coarse Dirichlet rows set to 0
+ * (alg:mg line 4; P = finite-element interpolation).
+ * `level` is the FINE level (>= 1). */
+int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream);
+
+/* x_fine += P e_coarse (alg:mg line 9).  `level` is the FINE level. */
+int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double* x_fine, void* stream);
+
+/* x = A_0^+ b on level 0 (minimum-norm, reading 3); Dirichlet
+ * entries of x set to 0. */
+int svk_coarse_solve(svk_ctx* ctx, const double* b, double* x, void* stream);
+
+/* One V(nu_pre, nu_post) cycle (alg:mg) on the finest level; x is
+ * in/out (a preconditioner application passes x = 0).  b and x must not alias. */
+int svk_vcycle(svk_ctx* ctx, const double* b, double* x, void* stream);
+
+/* Flexible GMRES, right-preconditioned by one V-cycle per iteration (P:127,
+ * P:649), no restart, stop when the Givens residual estimate <= rtol * ||r0||.
+ * x: in = x0 (boundary data in its Dirichlet entries), out = solution.
+ * hist (optional, host, maxit+1 doubles): relative residual estimate per
+ * iteration.  rep (optional, host) receives the report.  Returns SVK_OK,
+ * SVK_NOT_CONVERGED or an error. */
+int svk_fgmres(svk_ctx* ctx, const double* b, double* x, double rtol, int32_t maxit, double* hist,
+               svk_report* rep, void* stream);
+
+/* End-to-end solve through HOST buffers (pinned or pageable), each in the
+ * COMPACT layout [u_x (2N+1)^2, u_y (2N+1)^2, p (N+1)^2] of the finest level:
+ * copies b and x0 to the device, runs svk_fgmres, copies x back. */
+int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, double* x_host, double rtol,
+                   int32_t maxit, svk_report* rep, void* stream);
+
+/* Introspection for tests: the dense inverse of patch group (cat_x, cat_y),
+ * cat in {0: k=0, 1: k=1, 2: 2<=k<=N-2, 3: k=N-1, 4: k=N}, on `level`,
+ * copied to host `out` (n*n doubles, row-major, n <= 51); *n receives the
+ * number of patch unknowns.  Patch-local order: u_x window points (y outer,
+ * x inner; Dirichlet points skipped), then u_y, then p. */
+int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y, double* out, int32_t* n);
+
+/* Number of kernel launches issued by this context since creation (for the
+ * benchmark's gpu_launches count). */
+int64_t svk_launch_count(const svk_ctx* ctx);
+
+const char* svk_status_string(int status);
+const char* svk_last_error(const svk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVK_H_ */

@@ -1,0 +1,823 @@
+// svk.cu -- libsvk: C-ABI host side (hierarchy, V-cycle, FGMRES) and the single
+// translation unit that includes every kernel.  See include/svk.h for the API
+// contract and DESIGN.md for the design.
+#include "../../include/svk.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "stencil.cuh"
+#include "kernels_common.cuh"
+#include "krylov.cuh"
+#include "sweep_fused.cuh"
+
+using namespace svk;
+
+struct svk_ctx {
+  svk_config cfg{};
+  int nlev = 0;
+  std::vector<LevelGeom> g;
+  int* d_Ns = nullptr;
+  double* d_inv = nullptr;  // nlev * 25 padded 51x51 group inverses
+  double* d_fac = nullptr;  // nlev * FusedFactors (structured factors for the fused sweep)
+  std::vector<FusedFactors> h_fac;  // host copy, passed to the fused kernel by value (param space)
+  int nsm = 148;
+  // level 0 solve
+  double* d_cmat = nullptr;
+  int* d_cidx = nullptr;
+  int cni = 0;
+  // per-level workspaces
+  std::vector<double*> ws_x, ws_t, ws_r, ws_b;
+  double* d_dbuf = nullptr;  // packed patch buffer (unfused sweep), finest-level size
+  double* d_sw = nullptr;    // extra ping-pong vector for nsweeps > 1, finest-level size
+  // Krylov
+  std::vector<double*> V, Z;
+  double* d_w = nullptr;
+  double* d_r = nullptr;
+  double* d_part = nullptr;
+  double* d_coef = nullptr;
+  double* h_pin = nullptr;
+  int coef_cap = 0;
+  double* d_hb = nullptr;  // e2e staging
+  double* d_hx = nullptr;
+  cudaEvent_t ev[4]{};
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+constexpr int kDotBlocks = 148 * 4;
+
+std::mutex g_tab_mu;
+bool g_tab_done[64] = {false};
+
+int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+
+LevelGeom make_geom(int N) {
+  LevelGeom g{};
+  g.N = N;
+  g.lat = 2 * N + 1;
+  g.pu = round_up(g.lat, 8);
+  g.pp = round_up(N + 1, 8);
+  const int64_t plane = round_up((int64_t)g.lat * g.pu, 32);
+  g.oux = 0;
+  g.ouy = plane;
+  g.op = 2 * plane;
+  g.len = g.op + round_up((int64_t)(N + 1) * g.pp, 32);
+  g.h = 1.0 / N;
+  return g;
+}
+
+// Stencil tables from the exact 1D element matrices (stencil.cuh header).
+// 1D global matrices are assembled on a small grid and their generic rows and
+// columns read off; uniformity of every non-Dirichlet row/column is asserted.
+bool build_tables(StencilConst& t, std::string& err) {
+  const double K[3][3] = {{7, -8, 1}, {-8, 16, -8}, {1, -8, 7}};
+  const double M[3][3] = {{4, 2, -1}, {2, 16, 2}, {-1, 2, 4}};
+  const double Cm[2][3] = {{1, 2, 0}, {0, 2, 1}};
+  const double G[2][3] = {{-5, 4, 1}, {-1, -4, 5}};
+  std::memset(&t, 0, sizeof(t));
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      t.Khat[a][b] = K[a][b] / 3.0;
+      t.Mhat[a][b] = M[a][b] / 30.0;
+    }
+  for (int c = 0; c < 2; ++c)
+    for (int a = 0; a < 3; ++a) {
+      t.Chat[c][a] = Cm[c][a] / 6.0;
+      t.Ge[c][a] = G[c][a] / 6.0;
+    }
+  const int N = 8, lat = 2 * N + 1;
+  std::vector<double> k1(lat * lat, 0), m1(lat * lat, 0), c1((N + 1) * lat, 0), g1((N + 1) * lat, 0);
+  for (int e = 0; e < N; ++e)
+    for (int a = 0; a < 3; ++a) {
+      for (int b = 0; b < 3; ++b) {
+        k1[(2 * e + a) * lat + 2 * e + b] += t.Khat[a][b];
+        m1[(2 * e + a) * lat + 2 * e + b] += t.Mhat[a][b];
+      }
+      for (int c = 0; c < 2; ++c) {
+        c1[(e + c) * lat + 2 * e + a] += t.Chat[c][a];
+        g1[(e + c) * lat + 2 * e + a] += t.Ge[c][a];
+      }
+    }
+  auto at = [&](const std::vector<double>& v, int r, int c, int ncol) {
+    return (c < 0 || c >= ncol) ? 0.0 : v[r * ncol + c];
+  };
+  for (int i = 1; i < lat - 1; ++i) {
+    const int par = i & 1;
+    for (int o = -2; o <= 2; ++o) {
+      const double kv = at(k1, i, i + o, lat), mv = at(m1, i, i + o, lat);
+      if (i == 4 || i == 5) {
+        t.KR[par][o + 2] = kv;
+        t.MR[par][o + 2] = mv;
+      } else if (kv != t.KR[par][o + 2] && i > 5) {
+        err = "stencil rows not uniform";
+        return false;
+      }
+    }
+  }
+  for (int k = 0; k <= N; ++k) {
+    const int cls = k == 0 ? 0 : (k == N ? 2 : 1);
+    for (int o = 0; o < 5; ++o) {
+      t.CR[cls][o] = at(c1, k, 2 * k - 2 + o, lat);
+      t.GR[cls][o] = at(g1, k, 2 * k - 2 + o, lat);
+    }
+  }
+  // columns at non-Dirichlet lattice points (checked uniform)
+  for (int i = 1; i < lat - 1; ++i) {
+    const int par = i & 1;
+    const int k0 = par ? (i - 1) / 2 : i / 2 - 1, nk = par ? 2 : 3;
+    for (int q = 0; q < nk; ++q) {
+      const double cv = c1[(k0 + q) * lat + i], gv = g1[(k0 + q) * lat + i];
+      if (i <= 2) {
+        t.CC[par][q] = cv;
+        t.GC[par][q] = gv;
+      } else if (cv != t.CC[par][q] || gv != t.GC[par][q]) {
+        err = "stencil columns not uniform";
+        return false;
+      }
+    }
+  }
+  // the fused sweep visits only the structurally non-zero taps; check them here
+  const bool zeros_ok = t.KR[1][0] == 0 && t.KR[1][4] == 0 && t.MR[1][0] == 0 && t.MR[1][4] == 0 &&
+                        t.CC[0][0] == 0 && t.CC[0][2] == 0 && t.GC[0][1] == 0 && t.CR[1][0] == 0 &&
+                        t.CR[1][4] == 0 && t.GR[1][2] == 0;
+  if (!zeros_ok) {
+    err = "unexpected stencil sparsity";
+    return false;
+  }
+  return true;
+}
+
+#define CK(call)                                                             \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);        \
+      return SVK_ERR_CUDA;                                                   \
+    }                                                                        \
+  } while (0)
+#define CKL()                                                                \
+  do {                                                                       \
+    ctx->launches++;                                                         \
+    cudaError_t e_ = cudaGetLastError();                                     \
+    if (e_ != cudaSuccess) {                                                 \
+      ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);   \
+      return SVK_ERR_CUDA;                                                   \
+    }                                                                        \
+  } while (0)
+#define TRY(expr)                 \
+  do {                            \
+    int s_ = (expr);              \
+    if (s_ < 0) return s_;        \
+  } while (0)
+
+dim3 plane_grid(const LevelGeom& g) {
+  return dim3((unsigned)((g.pu + 31) / 32), (unsigned)((g.lat + 7) / 8), 3);
+}
+const dim3 kPlaneBlock(32, 8, 1);
+
+int valid_level(svk_ctx* ctx, int level) {
+  if (!ctx) return SVK_ERR_INVALID;
+  if (level < 0 || level >= ctx->nlev) {
+    ctx->err = "level out of range";
+    return SVK_ERR_INVALID;
+  }
+  return SVK_OK;
+}
+int valid_ptr(svk_ctx* ctx, const void* p, const char* what) {
+  if (!p || ((uintptr_t)p & 15u)) {
+    ctx->err = std::string(what) + ": NULL or not 16-byte aligned";
+    return SVK_ERR_INVALID;
+  }
+  return SVK_OK;
+}
+
+int alloc_vec(svk_ctx* ctx, double** p, int64_t n) {
+  CK(cudaMalloc(p, n * sizeof(double)));
+  CK(cudaMemset(*p, 0, n * sizeof(double)));
+  return SVK_OK;
+}
+
+// ------------------------------------------------------------------ level ops
+int op_residual(svk_ctx* ctx, int l, const double* x, const double* b, double* r, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  if (b) k_residual<true><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.nu, x, b, r);
+  else k_residual<false><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.nu, x, nullptr, r);
+  CKL();
+  return SVK_OK;
+}
+
+int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
+  if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
+    TRY(launch_fused_sweep(g, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l], ctx->d_inv + (size_t)l * 25 * kGroupStride,
+                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s));
+    CKL();
+    return SVK_OK;
+  }
+  // unfused: residual, packed patch solves, gather update
+  double* r = ctx->ws_r[l];
+  if (x_zero) {  // "initial approximation ... a zero vector": make the input really zero
+    CK(cudaMemsetAsync(const_cast<double*>(xin), 0, g.len * sizeof(double), s));
+  }
+  TRY(op_residual(ctx, l, xin, b, r, s));
+  const int64_t np = (int64_t)(g.N + 1) * (g.N + 1);
+  k_patch_solve_unfused<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(g, r, ctx->d_inv + (size_t)l * 25 * kGroupStride,
+                                                                     ctx->d_dbuf);
+  CKL();
+  k_vanka_update<<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.omega_v, scalar_w, xin, ctx->d_dbuf, xout);
+  CKL();
+  return SVK_OK;
+}
+
+int op_restrict(svk_ctx* ctx, int l, const double* rf, double* rc, cudaStream_t s) {
+  k_restrict<<<plane_grid(ctx->g[l - 1]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], rf, rc);
+  CKL();
+  return SVK_OK;
+}
+int op_prolong_add(svk_ctx* ctx, int l, const double* ec, double* xf, cudaStream_t s) {
+  k_prolong_add<<<plane_grid(ctx->g[l]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], ec, xf);
+  CKL();
+  return SVK_OK;
+}
+int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[0];
+  if (ctx->cfg.coarse == SVK_COARSE_SWEEPS3) {
+    // three relaxation sweeps from zero, ping-pong x <-> ws_t[0]
+    TRY(op_sweep(ctx, 0, x, b, ctx->ws_t[0], true, s));
+    TRY(op_sweep(ctx, 0, ctx->ws_t[0], b, x, false, s));
+    TRY(op_sweep(ctx, 0, x, b, ctx->ws_t[0], false, s));
+    CK(cudaMemcpyAsync(x, ctx->ws_t[0], g.len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return SVK_OK;
+  }
+  CK(cudaMemsetAsync(x, 0, g.len * sizeof(double), s));
+  k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_cmat, ctx->cni, ctx->d_cidx, b, x);
+  CKL();
+  return SVK_OK;
+}
+
+// alg:mg on level l; x in/out; x_zero: x is known to be 0 on entry
+int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  if (l == 0) return op_coarse(ctx, b, x, s);
+  double* cur = x;
+  double* oth = ctx->ws_t[l];
+  for (int k = 0; k < ctx->cfg.nu_pre; ++k) {  // "Relax on u_l and p_l"
+    TRY(op_sweep(ctx, l, cur, b, oth, x_zero && k == 0, s));
+    std::swap(cur, oth);
+  }
+  if (ctx->cfg.nu_pre == 0 && x_zero) CK(cudaMemsetAsync(cur, 0, g.len * sizeof(double), s));
+  TRY(op_residual(ctx, l, cur, b, ctx->ws_r[l], s));          // "Compute residual"
+  TRY(op_restrict(ctx, l, ctx->ws_r[l], ctx->ws_b[l - 1], s)); // "Restriction"
+  TRY(op_mg(ctx, l - 1, ctx->ws_b[l - 1], ctx->ws_x[l - 1], true, s));  // A_0^{-1} or MG(l-1)
+  TRY(op_prolong_add(ctx, l, ctx->ws_x[l - 1], cur, s));       // "Correction"
+  for (int k = 0; k < ctx->cfg.nu_post; ++k) {                 // "Relax on u_l and p_l"
+    TRY(op_sweep(ctx, l, cur, b, oth, false, s));
+    std::swap(cur, oth);
+  }
+  if (cur != x) CK(cudaMemcpyAsync(x, cur, g.len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return SVK_OK;
+}
+
+// out[0..m) = V[i]^T w  (deterministic), written to d_coef + off
+int op_dots(svk_ctx* ctx, const std::vector<const double*>& vs, const double* w, int64_t n, int off, cudaStream_t s) {
+  for (size_t g0 = 0; g0 < vs.size(); g0 += kMaxM) {
+    VecPtrs p{};
+    const int m = (int)std::min<size_t>(kMaxM, vs.size() - g0);
+    for (int q = 0; q < m; ++q) p.p[q] = vs[g0 + q];
+    if (m == 1) k_multidot<1><<<kDotBlocks, kRedThreads, 0, s>>>(p, 1, w, n, ctx->d_part);
+    else if (m <= 4) k_multidot<4><<<kDotBlocks, kRedThreads, 0, s>>>(p, m, w, n, ctx->d_part);
+    else k_multidot<8><<<kDotBlocks, kRedThreads, 0, s>>>(p, m, w, n, ctx->d_part);
+    CKL();
+    k_reduce_partials<<<m, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + off + g0, 0);
+    CKL();
+  }
+  return SVK_OK;
+}
+int op_axpys(svk_ctx* ctx, double* w, const std::vector<const double*>& vs, int off, double sign, int64_t n,
+             cudaStream_t s) {
+  for (size_t g0 = 0; g0 < vs.size(); g0 += kMaxM) {
+    VecPtrs p{};
+    const int m = (int)std::min<size_t>(kMaxM, vs.size() - g0);
+    for (int q = 0; q < m; ++q) p.p[q] = vs[g0 + q];
+    k_multiaxpy<<<kDotBlocks, 256, 0, s>>>(w, p, m, ctx->d_coef + off + g0, sign, n);
+    CKL();
+  }
+  return SVK_OK;
+}
+int ensure_coef(svk_ctx* ctx, int need) {
+  if (need <= ctx->coef_cap) return SVK_OK;
+  int cap = std::max(need, 2 * ctx->coef_cap);
+  if (ctx->d_coef) cudaFree(ctx->d_coef);
+  if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  CK(cudaMalloc(&ctx->d_coef, cap * sizeof(double)));
+  CK(cudaMallocHost(&ctx->h_pin, cap * sizeof(double)));
+  ctx->coef_cap = cap;
+  return SVK_OK;
+}
+int host_norm(svk_ctx* ctx, const double* v, int64_t n, double* out, cudaStream_t s) {
+  TRY(op_dots(ctx, {v}, v, n, 0, s));
+  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *out = std::sqrt(ctx->h_pin[0]);
+  return SVK_OK;
+}
+
+int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit, double* hist, svk_report* rep,
+                cudaStream_t s) {
+  auto t0 = std::chrono::steady_clock::now();
+  const int L = ctx->nlev - 1;
+  const LevelGeom& g = ctx->g[L];
+  const int64_t n = g.len;
+  svk_report R{};
+  double tv = 0, to = 0;
+  TRY(ensure_coef(ctx, 3 * (maxit + 2) + 8));
+  if (!ctx->d_r) TRY(alloc_vec(ctx, &ctx->d_r, n));
+  if (!ctx->d_w) TRY(alloc_vec(ctx, &ctx->d_w, n));
+  TRY(op_residual(ctx, L, x, b, ctx->d_r, s));
+  double beta;
+  TRY(host_norm(ctx, ctx->d_r, n, &beta, s));
+  if (hist) hist[0] = 1.0;
+  if (!std::isfinite(beta)) {
+    ctx->err = "non-finite initial residual";
+    return SVK_ERR_NONFINITE;
+  }
+  int status = SVK_OK, k = 0;
+  bool conv = beta == 0.0;
+  std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), gv(maxit + 1, 0.0);
+  auto Hij = [&](int i, int j) -> double& { return H[(size_t)i * maxit + j]; };
+  if (!conv) {
+    gv[0] = beta;
+    if (ctx->V.empty()) {
+      double* p;
+      TRY(alloc_vec(ctx, &p, n));
+      ctx->V.push_back(p);
+    }
+    k_scale<<<kDotBlocks, 256, 0, s>>>(ctx->V[0], ctx->d_r, 1.0 / beta, n);
+    CKL();
+    const int o1 = 0, o2 = maxit + 1, on = 2 * (maxit + 1);
+    for (int j = 0; j < maxit; ++j) {
+      if ((int)ctx->Z.size() <= j) {
+        double* p;
+        TRY(alloc_vec(ctx, &p, n));
+        ctx->Z.push_back(p);
+      }
+      // z_j = M v_j : one V-cycle from zero
+      CK(cudaEventRecord(ctx->ev[0], s));
+      TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
+      CK(cudaEventRecord(ctx->ev[1], s));
+      // w = A z_j ; CGS2 against v_0..v_j ; ||w||
+      TRY(op_residual(ctx, L, ctx->Z[j], nullptr, ctx->d_w, s));
+      std::vector<const double*> vs(ctx->V.begin(), ctx->V.begin() + j + 1);
+      TRY(op_dots(ctx, vs, ctx->d_w, n, o1, s));
+      TRY(op_axpys(ctx, ctx->d_w, vs, o1, -1.0, n, s));
+      TRY(op_dots(ctx, vs, ctx->d_w, n, o2, s));
+      TRY(op_axpys(ctx, ctx->d_w, vs, o2, -1.0, n, s));
+      TRY(op_dots(ctx, {ctx->d_w}, ctx->d_w, n, on, s));
+      CK(cudaEventRecord(ctx->ev[2], s));
+      CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (3 * (maxit + 1)) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      float a01 = 0, a12 = 0;
+      cudaEventElapsedTime(&a01, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&a12, ctx->ev[1], ctx->ev[2]);
+      tv += a01 * 1e-3;
+      to += a12 * 1e-3;
+      for (int i = 0; i <= j; ++i) Hij(i, j) = ctx->h_pin[o1 + i] + ctx->h_pin[o2 + i];
+      const double hn = std::sqrt(std::max(ctx->h_pin[on], 0.0));
+      if (!std::isfinite(hn)) {
+        status = SVK_ERR_NONFINITE;
+        ctx->err = "non-finite Arnoldi vector";
+        k = j;
+        break;
+      }
+      Hij(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
+        Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
+        Hij(i, j) = t;
+      }
+      const double a = Hij(j, j), bb = Hij(j + 1, j), rr = std::hypot(a, bb);
+      cs[j] = a / rr;
+      sn[j] = bb / rr;
+      Hij(j, j) = rr;
+      Hij(j + 1, j) = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      const double est = std::fabs(gv[j + 1]) / beta;
+      if (hist) hist[j + 1] = est;
+      k = j + 1;
+      if (est <= rtol || hn == 0.0) {
+        conv = true;
+        break;
+      }
+      if ((int)ctx->V.size() <= j + 1) {
+        double* p;
+        TRY(alloc_vec(ctx, &p, n));
+        ctx->V.push_back(p);
+      }
+      k_scale<<<kDotBlocks, 256, 0, s>>>(ctx->V[j + 1], ctx->d_w, 1.0 / hn, n);
+      CKL();
+    }
+    if (k > 0) {
+      std::vector<double> y(k);
+      for (int i = k - 1; i >= 0; --i) {
+        double t = gv[i];
+        for (int m = i + 1; m < k; ++m) t -= Hij(i, m) * y[m];
+        y[i] = t / Hij(i, i);
+      }
+      std::memcpy(ctx->h_pin, y.data(), k * sizeof(double));
+      CK(cudaMemcpyAsync(ctx->d_coef, ctx->h_pin, k * sizeof(double), cudaMemcpyHostToDevice, s));
+      std::vector<const double*> zs(ctx->Z.begin(), ctx->Z.begin() + k);
+      TRY(op_axpys(ctx, x, zs, 0, 1.0, n, s));
+    }
+  }
+  double rn = 0.0;
+  if (beta > 0) {
+    TRY(op_residual(ctx, L, x, b, ctx->d_r, s));
+    TRY(host_norm(ctx, ctx->d_r, n, &rn, s));
+  }
+  R.iterations = k;
+  R.converged = conv ? 1 : 0;
+  R.rel_residual = beta > 0 ? rn / beta : 0.0;
+  R.t_vcycle_s = tv;
+  R.t_orth_s = to;
+  R.t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (status == SVK_OK && !conv) status = SVK_NOT_CONVERGED;
+  if (status == SVK_OK && !std::isfinite(R.rel_residual)) status = SVK_ERR_NONFINITE;
+  R.status = status;
+  if (rep) *rep = R;
+  return status;
+}
+
+int free_ctx(svk_ctx* ctx) {
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(ctx->d_Ns);
+  F(ctx->d_inv);
+  F(ctx->d_fac);
+  F(ctx->d_cmat);
+  F(ctx->d_cidx);
+  for (auto* v : {&ctx->ws_x, &ctx->ws_t, &ctx->ws_r, &ctx->ws_b})
+    for (double* p : *v) F(p);
+  F(ctx->d_dbuf);
+  F(ctx->d_sw);
+  for (double* p : ctx->V) F(p);
+  for (double* p : ctx->Z) F(p);
+  F(ctx->d_w);
+  F(ctx->d_r);
+  F(ctx->d_part);
+  F(ctx->d_coef);
+  F(ctx->d_hb);
+  F(ctx->d_hx);
+  if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+  return SVK_OK;
+}
+
+int create_impl(svk_ctx* ctx) {
+  const svk_config& c = ctx->cfg;
+  CK(cudaSetDevice(c.device));
+  {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    if (c.device < 0 || c.device >= 64) {
+      ctx->err = "device ordinal out of range";
+      return SVK_ERR_INVALID;
+    }
+    if (!g_tab_done[c.device]) {
+      StencilConst t;
+      if (!build_tables(t, ctx->err)) return SVK_ERR_INVALID;
+      CK(cudaMemcpyToSymbol(c_st, &t, sizeof(t)));
+      g_tab_done[c.device] = true;
+    }
+  }
+  // hierarchy N0, 2 N0, ..., N (level 0 coarsest)
+  std::vector<int> Ns;
+  for (int N = c.n_coarse; N <= c.n_elem; N *= 2) Ns.push_back(N);
+  ctx->nlev = (int)Ns.size();
+  for (int N : Ns) ctx->g.push_back(make_geom(N));
+  CK(cudaMalloc(&ctx->d_Ns, Ns.size() * sizeof(int)));
+  CK(cudaMemcpy(ctx->d_Ns, Ns.data(), Ns.size() * sizeof(int), cudaMemcpyHostToDevice));
+  for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ctx->ev[k]));
+  // patch setup: 25 groups x levels, one CTA each
+  int* d_status;
+  CK(cudaMalloc(&d_status, sizeof(int)));
+  CK(cudaMemset(d_status, 0, sizeof(int)));
+  CK(cudaMalloc(&ctx->d_inv, (size_t)ctx->nlev * 25 * kGroupStride * sizeof(double)));
+  k_patch_setup<<<dim3(25, ctx->nlev), 256>>>(ctx->d_Ns, c.nu, ctx->d_inv, d_status);
+  CKL();
+  CK(cudaMalloc(&ctx->d_fac, (size_t)ctx->nlev * kFacStride * sizeof(double)));
+  TRY(launch_factor_setup(ctx->d_Ns, ctx->nlev, c.nu, ctx->d_inv, ctx->d_fac, d_status));
+  CKL();
+  // level-0 bordered pseudo-inverse
+  const LevelGeom& g0 = ctx->g[0];
+  std::vector<int> idx;
+  for (int comp = 0; comp < 2; ++comp)
+    for (int j = 1; j < g0.lat - 1; ++j)
+      for (int i = 1; i < g0.lat - 1; ++i) idx.push_back((int)((comp ? g0.ouy : g0.oux) + (int64_t)j * g0.pu + i));
+  for (int ky = 0; ky <= g0.N; ++ky)
+    for (int kx = 0; kx <= g0.N; ++kx) idx.push_back((int)p_at(g0, kx, ky));
+  ctx->cni = (int)idx.size();
+  const int nb = ctx->cni + 1;
+  CK(cudaMalloc(&ctx->d_cidx, idx.size() * sizeof(int)));
+  CK(cudaMemcpy(ctx->d_cidx, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->d_cmat, (size_t)nb * nb * sizeof(double)));
+  k_coarse_build<<<nb, 128>>>(g0, c.nu, ctx->d_cidx, ctx->cni, ctx->d_cmat);
+  CKL();
+  int* d_perm;
+  double* d_colk;
+  CK(cudaMalloc(&d_perm, nb * sizeof(int)));
+  CK(cudaMalloc(&d_colk, nb * sizeof(double)));
+  k_coarse_invert<<<1, 256>>>(ctx->d_cmat, nb, d_perm, d_colk, d_status);
+  CKL();
+  int hs = 0;
+  CK(cudaMemcpy(&hs, d_status, sizeof(int), cudaMemcpyDeviceToHost));
+  ctx->h_fac.resize(ctx->nlev);
+  CK(cudaMemcpy(ctx->h_fac.data(), ctx->d_fac, (size_t)ctx->nlev * sizeof(FusedFactors), cudaMemcpyDeviceToHost));
+  CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, c.device));
+  cudaFree(d_perm);
+  cudaFree(d_colk);
+  cudaFree(d_status);
+  if (hs) {
+    ctx->err = "singular patch or coarse matrix";
+    return SVK_ERR_SINGULAR;
+  }
+  // workspaces
+  ctx->ws_x.assign(ctx->nlev, nullptr);
+  ctx->ws_t.assign(ctx->nlev, nullptr);
+  ctx->ws_r.assign(ctx->nlev, nullptr);
+  ctx->ws_b.assign(ctx->nlev, nullptr);
+  for (int l = 0; l < ctx->nlev; ++l) {
+    const int64_t n = ctx->g[l].len;
+    if (l < ctx->nlev - 1) {
+      TRY(alloc_vec(ctx, &ctx->ws_x[l], n));
+      TRY(alloc_vec(ctx, &ctx->ws_b[l], n));
+    }
+    TRY(alloc_vec(ctx, &ctx->ws_t[l], n));
+    TRY(alloc_vec(ctx, &ctx->ws_r[l], n));
+  }
+  if (c.sweep_impl == SVK_SWEEP_UNFUSED) {
+    const LevelGeom& gf = ctx->g.back();
+    TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
+  }
+  CK(cudaMalloc(&ctx->d_part, (size_t)kMaxM * kDotBlocks * sizeof(double)));
+  CK(cudaDeviceSynchronize());
+  return SVK_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+int svk_config_default(svk_config* cfg, int32_t n_elem) {
+  if (!cfg) return SVK_ERR_INVALID;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->n_elem = n_elem;
+  cfg->n_coarse = 4;
+  cfg->nu = 1.0;
+  cfg->omega_v = 0.8;
+  cfg->weighting = SVK_WEIGHT_MULT;
+  cfg->nu_pre = 1;
+  cfg->nu_post = 1;
+  cfg->coarse = SVK_COARSE_EXACT;
+  cfg->sweep_impl = SVK_SWEEP_FUSED;
+  cfg->device = 0;
+  return SVK_OK;
+}
+
+int svk_create(const svk_config* cfg, svk_ctx** out) {
+  if (!out) return SVK_ERR_INVALID;
+  *out = nullptr;
+  if (!cfg) return SVK_ERR_INVALID;
+  if (cfg->n_coarse < 4 || cfg->n_elem < cfg->n_coarse || cfg->nu <= 0 || cfg->nu_pre < 0 || cfg->nu_post < 0 ||
+      cfg->n_elem > (1 << 15))
+    return SVK_ERR_INVALID;
+  int n = cfg->n_elem;
+  while (n > cfg->n_coarse) {
+    if (n % 2) return SVK_ERR_INVALID;
+    n /= 2;
+  }
+  if (n != cfg->n_coarse) return SVK_ERR_INVALID;
+  svk_ctx* ctx = new svk_ctx;
+  ctx->cfg = *cfg;
+  int st = create_impl(ctx);
+  if (st != SVK_OK) {
+    std::fprintf(stderr, "svk_create: %s\n", ctx->err.c_str());
+    free_ctx(ctx);
+    return st;
+  }
+  *out = ctx;
+  return SVK_OK;
+}
+
+int svk_destroy(svk_ctx* ctx) {
+  if (!ctx) return SVK_ERR_INVALID;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  return free_ctx(ctx);
+}
+
+int svk_num_levels(const svk_ctx* ctx, int32_t* levels) {
+  if (!ctx || !levels) return SVK_ERR_INVALID;
+  *levels = ctx->nlev;
+  return SVK_OK;
+}
+
+int svk_level_info(const svk_ctx* ctx, int32_t level, svk_level* out) {
+  if (!ctx || !out || level < 0 || level >= ctx->nlev) return SVK_ERR_INVALID;
+  const LevelGeom& g = ctx->g[level];
+  out->N = g.N;
+  out->lat = g.lat;
+  out->vec_len = g.len;
+  out->off_ux = g.oux;
+  out->off_uy = g.ouy;
+  out->off_p = g.op;
+  out->pitch_u = g.pu;
+  out->pitch_p = g.pp;
+  out->n_dof = 2 * (int64_t)g.lat * g.lat + (int64_t)(g.N + 1) * (g.N + 1);
+  out->n_patch = (int64_t)(g.N + 1) * (g.N + 1);
+  return SVK_OK;
+}
+
+int svk_set_problem(svk_ctx* ctx, int32_t level, int32_t kind, double* b, double* x0, void* stream) {
+  TRY(valid_level(ctx, level));
+  if (kind < 0 || kind > 3) return SVK_ERR_INVALID;
+  if (b) TRY(valid_ptr(ctx, b, "b"));
+  if (x0) TRY(valid_ptr(ctx, x0, "x0"));
+  const LevelGeom& g = ctx->g[level];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (b) CK(cudaMemsetAsync(b, 0, g.len * sizeof(double), s));
+  if (x0) CK(cudaMemsetAsync(x0, 0, g.len * sizeof(double), s));
+  k_set_problem<<<plane_grid(g), kPlaneBlock, 0, s>>>(g, kind, ctx->cfg.nu, b, x0);
+  CKL();
+  return SVK_OK;
+}
+
+int svk_residual(svk_ctx* ctx, int32_t level, const double* x, const double* b, double* r, void* stream) {
+  TRY(valid_level(ctx, level));
+  TRY(valid_ptr(ctx, x, "x"));
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, r, "r"));
+  return op_residual(ctx, level, x, b, r, (cudaStream_t)stream);
+}
+
+int svk_matvec(svk_ctx* ctx, int32_t level, const double* x, double* y, void* stream) {
+  TRY(valid_level(ctx, level));
+  TRY(valid_ptr(ctx, x, "x"));
+  TRY(valid_ptr(ctx, y, "y"));
+  return op_residual(ctx, level, x, nullptr, y, (cudaStream_t)stream);
+}
+
+int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, int32_t nsweeps,
+                    void* stream) {
+  TRY(valid_level(ctx, level));
+  TRY(valid_ptr(ctx, x_in, "x_in"));
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, x_out, "x_out"));
+  if (nsweeps < 1 || x_in == x_out || b == x_out) {
+    ctx->err = "nsweeps < 1 or aliasing x_out";
+    return SVK_ERR_INVALID;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const LevelGeom& g = ctx->g[level];
+  if (ctx->cfg.sweep_impl == SVK_SWEEP_UNFUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
+  if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);
+  if (!ctx->d_sw) TRY(alloc_vec(ctx, &ctx->d_sw, ctx->g.back().len));
+  // ping-pong so that the last sweep lands in x_out
+  double* bufs[2] = {x_out, ctx->d_sw};
+  int dst = (nsweeps % 2 == 1) ? 0 : 1;
+  const double* cur = x_in;
+  for (int k = 0; k < nsweeps; ++k) {
+    TRY(op_sweep(ctx, level, cur, b, bufs[dst], false, s));
+    cur = bufs[dst];
+    dst ^= 1;
+  }
+  (void)g;
+  return SVK_OK;
+}
+
+int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream) {
+  TRY(valid_level(ctx, level));
+  if (level < 1) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, r_fine, "r_fine"));
+  TRY(valid_ptr(ctx, r_coarse, "r_coarse"));
+  return op_restrict(ctx, level, r_fine, r_coarse, (cudaStream_t)stream);
+}
+
+int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double* x_fine, void* stream) {
+  TRY(valid_level(ctx, level));
+  if (level < 1) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, e_coarse, "e_coarse"));
+  TRY(valid_ptr(ctx, x_fine, "x_fine"));
+  return op_prolong_add(ctx, level, e_coarse, x_fine, (cudaStream_t)stream);
+}
+
+int svk_coarse_solve(svk_ctx* ctx, const double* b, double* x, void* stream) {
+  if (!ctx) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, x, "x"));
+  return op_coarse(ctx, b, x, (cudaStream_t)stream);
+}
+
+int svk_vcycle(svk_ctx* ctx, const double* b, double* x, void* stream) {
+  if (!ctx) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, x, "x"));
+  if (b == x) return SVK_ERR_INVALID;
+  return op_mg(ctx, ctx->nlev - 1, b, x, false, (cudaStream_t)stream);
+}
+
+int svk_fgmres(svk_ctx* ctx, const double* b, double* x, double rtol, int32_t maxit, double* hist, svk_report* rep,
+               void* stream) {
+  if (!ctx) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, x, "x"));
+  if (maxit < 1 || !(rtol >= 0) || b == x) return SVK_ERR_INVALID;
+  return fgmres_impl(ctx, b, x, rtol, maxit, hist, rep, (cudaStream_t)stream);
+}
+
+int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, double* x_host, double rtol,
+                   int32_t maxit, svk_report* rep, void* stream) {
+  if (!ctx || !b_host || !x0_host || !x_host) return SVK_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const LevelGeom& g = ctx->g.back();
+  if (!ctx->d_hb) TRY(alloc_vec(ctx, &ctx->d_hb, g.len));
+  if (!ctx->d_hx) TRY(alloc_vec(ctx, &ctx->d_hx, g.len));
+  const int64_t nv = (int64_t)g.lat * g.lat;
+  const size_t wu = g.lat * sizeof(double), wp = (g.N + 1) * sizeof(double);
+  for (int which = 0; which < 2; ++which) {
+    const double* src = which ? x0_host : b_host;
+    double* dst = which ? ctx->d_hx : ctx->d_hb;
+    CK(cudaMemcpy2DAsync(dst + g.oux, g.pu * sizeof(double), src, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpy2DAsync(dst + g.ouy, g.pu * sizeof(double), src + nv, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpy2DAsync(dst + g.op, g.pp * sizeof(double), src + 2 * nv, wp, wp, g.N + 1, cudaMemcpyHostToDevice, s));
+  }
+  int st = fgmres_impl(ctx, ctx->d_hb, ctx->d_hx, rtol, maxit, nullptr, rep, s);
+  if (st < 0) return st;
+  CK(cudaMemcpy2DAsync(x_host, wu, ctx->d_hx + g.oux, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpy2DAsync(x_host + nv, wu, ctx->d_hx + g.ouy, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpy2DAsync(x_host + 2 * nv, wp, ctx->d_hx + g.op, g.pp * sizeof(double), wp, g.N + 1,
+                       cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return st;
+}
+
+int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y, double* out, int32_t* n) {
+  TRY(valid_level(ctx, level));
+  if (cat_x < 0 || cat_x > 4 || cat_y < 0 || cat_y > 4 || !out || !n) return SVK_ERR_INVALID;
+  const LevelGeom& g = ctx->g[level];
+  std::vector<double> pad(kGroupStride);
+  CK(cudaMemcpy(pad.data(), ctx->d_inv + ((size_t)level * 25 + cat_y * 5 + cat_x) * kGroupStride,
+                kGroupStride * sizeof(double), cudaMemcpyDeviceToHost));
+  const int kx = cat_rep(cat_x, g.N), ky = cat_rep(cat_y, g.N);
+  std::vector<int> slots;
+  for (int comp = 0; comp < 2; ++comp)
+    for (int oy = 0; oy < 5; ++oy)
+      for (int ox = 0; ox < 5; ++ox) {
+        const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+        if (i < 1 || j < 1 || i > g.lat - 2 || j > g.lat - 2) continue;
+        slots.push_back(comp * 25 + oy * 5 + ox);
+      }
+  slots.push_back(50);
+  const int m = (int)slots.size();
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < m; ++c) out[r * m + c] = pad[slots[r] * kSlots + slots[c]];
+  *n = m;
+  return SVK_OK;
+}
+
+int64_t svk_launch_count(const svk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+const char* svk_status_string(int status) {
+  switch (status) {
+    case SVK_OK: return "ok";
+    case SVK_NOT_CONVERGED: return "not converged";
+    case SVK_ERR_INVALID: return "invalid argument";
+    case SVK_ERR_CUDA: return "CUDA error";
+    case SVK_ERR_NCCL: return "NCCL error";
+    case SVK_ERR_SINGULAR: return "singular factorisation";
+    case SVK_ERR_NONFINITE: return "non-finite value";
+    case SVK_ERR_ALLOC: return "allocation failed";
+    default: return "unknown status";
+  }
+}
+
+const char* svk_last_error(const svk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

@@ -1,0 +1,274 @@
+"""Thin ctypes binding of libsvk (include/svk.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of ``libsvk.so``.  PyTorch supplies device memory (float64 CUDA
+tensors in the pitched layout of ``svk_level_info``) and the current stream.
+There is no CPU fallback: if ``libsvk.so`` is missing or no CUDA device is
+present, construction fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsvk.so")
+
+SVK_OK, SVK_NOT_CONVERGED = 0, 1
+PROBLEMS = {"zero": 0, "mms_paper": 1, "mms_inspace": 2, "cavity": 3}
+WEIGHTING = {"mult": 0, "scalar": 1}
+COARSE = {"exact": 0, "sweeps3": 1}
+SWEEP = {"fused": 0, "unfused": 1}
+
+
+class SvkError(RuntimeError):
+    pass
+
+
+class Config(C.Structure):
+    _fields_ = [("n_elem", C.c_int32), ("n_coarse", C.c_int32), ("nu", C.c_double), ("omega_v", C.c_double),
+                ("weighting", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("coarse", C.c_int32),
+                ("sweep_impl", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32 * 8)]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [("N", C.c_int32), ("lat", C.c_int32), ("vec_len", C.c_int64), ("off_ux", C.c_int64),
+                ("off_uy", C.c_int64), ("off_p", C.c_int64), ("pitch_u", C.c_int64), ("pitch_p", C.c_int64),
+                ("n_dof", C.c_int64), ("n_patch", C.c_int64)]
+
+
+class Report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
+                ("rel_residual", C.c_double), ("t_total_s", C.c_double), ("t_vcycle_s", C.c_double),
+                ("t_orth_s", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_lib = None
+
+# every symbol declared in include/svk.h (tests check the export table against this)
+EXPORTS = {
+    "svk_config_default": (C.c_int, [C.POINTER(Config), C.c_int32]),
+    "svk_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
+    "svk_destroy": (C.c_int, [C.c_void_p]),
+    "svk_num_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "svk_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LevelInfo)]),
+    "svk_set_problem": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_residual": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_matvec": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_vanka_sweep": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "svk_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_prolong_add": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_coarse_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_vcycle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_fgmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
+                             C.POINTER(Report), C.c_void_p]),
+    "svk_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
+                                 C.POINTER(Report), C.c_void_p]),
+    "svk_patch_inverse": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
+    "svk_launch_count": (C.c_int64, [C.c_void_p]),
+    "svk_status_string": (C.c_char_p, [C.c_int]),
+    "svk_last_error": (C.c_char_p, [C.c_void_p]),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsvk.so (no compute).  Raises ImportError if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libsvk.so not built (%s); run `python -m paper_2401_06277_b200.build`" % path)
+    lib = C.CDLL(path)
+    for name, (res, args) in EXPORTS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _stream(torch):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Solver:
+    """One libsvk context: hierarchy N, N/2, ..., n_coarse on one CUDA device."""
+
+    def __init__(self, n_elem: int, n_coarse: int = 4, nu: float = 1.0, omega: float = 0.8,
+                 weighting: str = "mult", nu_pre: int = 1, nu_post: int = 1, coarse: str = "exact",
+                 sweep: str = "fused", device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise SvkError("libsvk needs a CUDA device (B200, sm_100a); none is visible")
+        self.torch = torch
+        self.lib = load_library()
+        cfg = Config()
+        self.lib.svk_config_default(C.byref(cfg), n_elem)
+        cfg.n_coarse, cfg.nu, cfg.omega_v = n_coarse, nu, omega
+        cfg.weighting, cfg.nu_pre, cfg.nu_post = WEIGHTING[weighting], nu_pre, nu_post
+        cfg.coarse, cfg.sweep_impl, cfg.device = COARSE[coarse], SWEEP[sweep], device
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        h = C.c_void_p()
+        st = self.lib.svk_create(C.byref(cfg), C.byref(h))
+        if st != SVK_OK:
+            raise SvkError("svk_create failed: %s" % self.lib.svk_status_string(st).decode())
+        self._h = h
+        nl = C.c_int32()
+        self.lib.svk_num_levels(self._h, C.byref(nl))
+        self.levels = nl.value
+        self.info = []
+        for l in range(self.levels):
+            li = LevelInfo()
+            self._chk(self.lib.svk_level_info(self._h, l, C.byref(li)))
+            self.info.append(li)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.svk_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ helpers
+    def _chk(self, st):
+        if st < 0:
+            msg = self.lib.svk_last_error(self._h)
+            raise SvkError("%s: %s" % (self.lib.svk_status_string(st).decode(), msg.decode() if msg else ""))
+        return st
+
+    @property
+    def fine(self) -> int:
+        return self.levels - 1
+
+    def _vec(self, t, level, name):
+        li = self.info[level]
+        if t.dtype != self.torch.float64 or not t.is_cuda or not t.is_contiguous() or t.numel() != li.vec_len:
+            raise SvkError("%s: expected a contiguous float64 CUDA tensor of %d elements" % (name, li.vec_len))
+        return C.c_void_p(t.data_ptr())
+
+    def new_vector(self, level: int | None = None):
+        level = self.fine if level is None else level
+        return self.torch.zeros(self.info[level].vec_len, dtype=self.torch.float64, device=self.device)
+
+    def planes(self, v, level: int | None = None):
+        """(ux, uy, p) views of a pitched vector, shapes (2N+1, 2N+1), (2N+1, 2N+1), (N+1, N+1)."""
+        level = self.fine if level is None else level
+        li = self.info[level]
+        n = li.lat
+        ux = v[li.off_ux:li.off_ux + n * li.pitch_u].view(n, li.pitch_u)[:, :n]
+        uy = v[li.off_uy:li.off_uy + n * li.pitch_u].view(n, li.pitch_u)[:, :n]
+        p = v[li.off_p:li.off_p + (li.N + 1) * li.pitch_p].view(li.N + 1, li.pitch_p)[:, :li.N + 1]
+        return ux, uy, p
+
+    def to_compact(self, v, level: int | None = None):
+        ux, uy, p = self.planes(v, level)
+        return self.torch.cat([ux.reshape(-1), uy.reshape(-1), p.reshape(-1)])
+
+    def from_compact(self, c, level: int | None = None):
+        level = self.fine if level is None else level
+        t = self.torch
+        c = t.as_tensor(np.asarray(c) if not isinstance(c, t.Tensor) else c, dtype=t.float64).to(self.device)
+        li = self.info[level]
+        nv = li.lat * li.lat
+        v = self.new_vector(level)
+        ux, uy, p = self.planes(v, level)
+        ux.copy_(c[:nv].view(li.lat, li.lat))
+        uy.copy_(c[nv:2 * nv].view(li.lat, li.lat))
+        p.copy_(c[2 * nv:].view(li.N + 1, li.N + 1))
+        return v
+
+    # ------------------------------------------------------------------ API
+    def set_problem(self, kind: str = "mms_paper", level: int | None = None):
+        level = self.fine if level is None else level
+        b, x0 = self.new_vector(level), self.new_vector(level)
+        self._chk(self.lib.svk_set_problem(self._h, level, PROBLEMS[kind], C.c_void_p(b.data_ptr()),
+                                           C.c_void_p(x0.data_ptr()), _stream(self.torch)))
+        return b, x0
+
+    def residual(self, level, x, b, out=None):
+        out = self.new_vector(level) if out is None else out
+        self._chk(self.lib.svk_residual(self._h, level, self._vec(x, level, "x"), self._vec(b, level, "b"),
+                                        self._vec(out, level, "r"), _stream(self.torch)))
+        return out
+
+    def matvec(self, level, x, out=None):
+        out = self.new_vector(level) if out is None else out
+        self._chk(self.lib.svk_matvec(self._h, level, self._vec(x, level, "x"), self._vec(out, level, "y"),
+                                      _stream(self.torch)))
+        return out
+
+    def sweep(self, level, x, b, nsweeps: int = 1, out=None):
+        out = self.new_vector(level) if out is None else out
+        self._chk(self.lib.svk_vanka_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
+                                           self._vec(out, level, "x_out"), nsweeps, _stream(self.torch)))
+        return out
+
+    def restrict(self, level, rf, out=None):
+        out = self.new_vector(level - 1) if out is None else out
+        self._chk(self.lib.svk_restrict(self._h, level, self._vec(rf, level, "r_fine"),
+                                        self._vec(out, level - 1, "r_coarse"), _stream(self.torch)))
+        return out
+
+    def prolong_add(self, level, ec, xf):
+        self._chk(self.lib.svk_prolong_add(self._h, level, self._vec(ec, level - 1, "e_coarse"),
+                                           self._vec(xf, level, "x_fine"), _stream(self.torch)))
+        return xf
+
+    def coarse_solve(self, b, out=None):
+        out = self.new_vector(0) if out is None else out
+        self._chk(self.lib.svk_coarse_solve(self._h, self._vec(b, 0, "b"), self._vec(out, 0, "x"),
+                                            _stream(self.torch)))
+        return out
+
+    def vcycle(self, b, x=None):
+        x = self.new_vector() if x is None else x
+        self._chk(self.lib.svk_vcycle(self._h, self._vec(b, self.fine, "b"), self._vec(x, self.fine, "x"),
+                                      _stream(self.torch)))
+        return x
+
+    def fgmres(self, b, x, rtol: float = 1e-10, maxit: int = 200):
+        """In-place on x.  Returns (report dict, history np.ndarray)."""
+        hist = np.zeros(maxit + 1)
+        rep = Report()
+        st = self._chk(self.lib.svk_fgmres(self._h, self._vec(b, self.fine, "b"), self._vec(x, self.fine, "x"),
+                                           rtol, maxit, hist.ctypes.data_as(C.c_void_p), C.byref(rep),
+                                           _stream(self.torch)))
+        d = rep.as_dict()
+        d["status"] = st
+        return d, hist[: rep.iterations + 1].copy()
+
+    def solve_host(self, b_host: np.ndarray, x0_host: np.ndarray, rtol: float = 1e-10, maxit: int = 200,
+                   x_host: np.ndarray | None = None):
+        """End-to-end solve from host arrays in the compact layout (svk_solve_host)."""
+        b_host = np.ascontiguousarray(b_host, dtype=np.float64)
+        x0_host = np.ascontiguousarray(x0_host, dtype=np.float64)
+        x_host = np.empty_like(b_host) if x_host is None else x_host
+        rep = Report()
+        st = self._chk(self.lib.svk_solve_host(self._h, b_host.ctypes.data_as(C.c_void_p),
+                                               x0_host.ctypes.data_as(C.c_void_p), x_host.ctypes.data_as(C.c_void_p),
+                                               rtol, maxit, C.byref(rep), _stream(self.torch)))
+        d = rep.as_dict()
+        d["status"] = st
+        return x_host, d
+
+    def patch_inverse(self, level: int, cat_x: int, cat_y: int) -> np.ndarray:
+        out = np.zeros(51 * 51)
+        n = C.c_int32()
+        self._chk(self.lib.svk_patch_inverse(self._h, level, cat_x, cat_y, out.ctypes.data_as(C.c_void_p),
+                                             C.byref(n)))
+        return out[: n.value * n.value].reshape(n.value, n.value).copy()
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.svk_launch_count(self._h))
