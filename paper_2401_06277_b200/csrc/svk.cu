@@ -37,6 +37,7 @@ struct svk_ctx {
   // per-level workspaces
   std::vector<double*> ws_x, ws_t, ws_r, ws_b;
   double* d_dbuf = nullptr;  // packed patch buffer (unfused sweep), finest-level size
+  double* d_bd = nullptr;    // boundary-patch corrections (fused sweep), finest-level size
   double* d_sw = nullptr;    // extra ping-pong vector for nsweeps > 1, finest-level size
   // Krylov
   std::vector<double*> V, Z;
@@ -221,9 +222,11 @@ int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
   const LevelGeom& g = ctx->g[l];
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
-    TRY(launch_fused_sweep(g, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l], ctx->d_inv + (size_t)l * 25 * kGroupStride,
-                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s));
+    TRY(launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
+                           ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_bd, x_zero ? nullptr : xin, b, xout,
+                           ctx->nsm, s));
     CKL();
+    ctx->launches++;  // two kernels: boundary patches + fused sweep
     return SVK_OK;
   }
   // unfused: residual, packed patch solves, gather update
@@ -472,6 +475,7 @@ int free_ctx(svk_ctx* ctx) {
   for (auto* v : {&ctx->ws_x, &ctx->ws_t, &ctx->ws_r, &ctx->ws_b})
     for (double* p : *v) F(p);
   F(ctx->d_dbuf);
+  F(ctx->d_bd);
   F(ctx->d_sw);
   for (double* p : ctx->V) F(p);
   for (double* p : ctx->Z) F(p);
@@ -569,6 +573,7 @@ int create_impl(svk_ctx* ctx) {
     TRY(alloc_vec(ctx, &ctx->ws_t[l], n));
     TRY(alloc_vec(ctx, &ctx->ws_r[l], n));
   }
+  TRY(alloc_vec(ctx, &ctx->d_bd, (int64_t)kSlots * bd_count(ctx->g.back().N)));
   if (c.sweep_impl == SVK_SWEEP_UNFUSED) {
     const LevelGeom& gf = ctx->g.back();
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));

@@ -163,6 +163,69 @@ __global__ void k_factor_setup(const int* __restrict__ Ns, double nu, double* __
 
 
 // =============================================================================
+// Boundary patches (some axis category != 2: kx or ky in {0, 1, N-1, N}).
+// They are only O(N) of the (N+1)^2 patches but have 24 different matrices
+// without the reflection symmetry, so they are solved up front by this small
+// kernel -- one CTA of 64 threads per patch: the 51 window residuals
+// (stencil from global memory), then one row of the dense padded group
+// inverse per thread -- and their corrections are stored slot-major in `bd`.
+// The fused kernel then loads them instead of diverging into a dense solve.
+// Boundary patch numbering: rows ky in {0,1,N-1,N} first (4 x (N+1)), then
+// columns kx in {0,1,N-1,N} for 2 <= ky <= N-2 (4 x (N-3)); nb = 8N - 8.
+// =============================================================================
+__host__ __device__ __forceinline__ int bd_axis(int k, int N) { return k <= 1 ? k : k - (N - 3); }
+__host__ __device__ __forceinline__ int64_t bd_count(int N) { return 8 * (int64_t)N - 8; }
+__host__ __device__ __forceinline__ int64_t bd_index(int kx, int ky, int N) {
+  if (ky <= 1 || ky >= N - 1) return (int64_t)bd_axis(ky, N) * (N + 1) + kx;
+  return 4 * (int64_t)(N + 1) + (int64_t)bd_axis(kx, N) * (N - 3) + (ky - 2);
+}
+
+__global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
+                                                        const double* __restrict__ x, const double* __restrict__ b,
+                                                        double* __restrict__ bd) {
+  const int N = g.N, lat = g.lat;
+  const int64_t nb = bd_count(N);
+  const int64_t id = blockIdx.x;
+  int kx, ky;
+  if (id < 4 * (int64_t)(N + 1)) {
+    const int r = (int)(id / (N + 1));
+    ky = r <= 1 ? r : r + N - 3;
+    kx = (int)(id % (N + 1));
+  } else {
+    const int64_t q = id - 4 * (int64_t)(N + 1);
+    const int c = (int)(q / (N - 3));
+    kx = c <= 1 ? c : c + N - 3;
+    ky = 2 + (int)(q % (N - 3));
+  }
+  __shared__ double rv[kSlots];
+  const int s = threadIdx.x;
+  if (s < kSlots) {
+    double r = 0.0;
+    if (s < 50) {
+      const int comp = s / 25, oy = (s % 25) / 5, ox = s % 5;
+      const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+      if (i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
+        const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
+        double ax = 0.0;
+        if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
+        r = b[o] - ax;
+      }
+    } else {
+      const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
+      r = b[p_at(g, kx, ky)] - ax;
+    }
+    rv[s] = r;
+  }
+  __syncthreads();
+  if (s < kSlots) {
+    const double* A = dinv + (size_t)(pcat(ky, N) * 5 + pcat(kx, N)) * kGroupStride + s * kSlots;
+    double d = 0.0;
+    for (int q = 0; q < kSlots; ++q) d = fma(A[q], rv[q], d);
+    bd[(int64_t)s * nb + bd_index(kx, ky, N)] = d;
+  }
+}
+
+// =============================================================================
 // Fused additive Vanka sweep (alg:vk) -- one kernel per sweep:
 //   x_out = x_in + W sum_i V_i^T A_i^{-1} V_i (b - A x_in)
 //
@@ -203,7 +266,7 @@ struct FusedArgs {
   double omega;
   int scalar_w;
   int chunk;            // node rows per CTA
-  const double* dinv;   // this level's 25 padded group inverses
+  const double* bd;     // boundary-patch corrections (k_boundary_patches), slot-major
   const double* xin;    // unused when the kernel is instantiated with XZERO
   const double* b;
   double* xout;
@@ -509,31 +572,6 @@ __device__ __forceinline__ double solve_generic(double (&vx)[25], double (&vy)[2
   return dp;
 }
 
-// Boundary-category patch: dense padded 51x51 group inverse (slot = comp*25+oy*5+ox, 50 = p)
-__device__ __noinline__ double solve_dense(double (&vx)[25], double (&vy)[25], double rp, const double* __restrict__ Ai) {
-  double r[51];
-#pragma unroll
-  for (int q = 0; q < 25; ++q) {
-    r[q] = vx[q];
-    r[25 + q] = vy[q];
-  }
-  r[50] = rp;
-  double out[51];
-#pragma unroll 1
-  for (int s = 0; s < 51; ++s) {
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < 51; ++q) acc = fma(__ldg(Ai + s * 51 + q), r[q], acc);
-    out[s] = acc;
-  }
-#pragma unroll
-  for (int q = 0; q < 25; ++q) {
-    vx[q] = out[q];
-    vy[q] = out[25 + q];
-  }
-  return out[50];
-}
-
 template <bool XZERO>
 __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F) {
   extern __shared__ double smem[];
@@ -605,8 +643,14 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
       const double rp = S.RP(s, t + 1);
       if (kxp >= 2 && kxp <= N - 2 && s >= 2 && s <= N - 2) {
         dp = solve_generic(vx, vy, rp, F);
-      } else {
-        dp = solve_dense(vx, vy, rp, A.dinv + (size_t)(pcat(s, N) * 5 + pcat(kxp, N)) * 2601);
+      } else {  // precomputed by k_boundary_patches
+        const int64_t nb = bd_count(N), bi = bd_index(kxp, s, N);
+#pragma unroll
+        for (int q = 0; q < 25; ++q) {
+          vx[q] = A.bd[q * nb + bi];
+          vy[q] = A.bd[(25 + q) * nb + bi];
+        }
+        dp = A.bd[50 * nb + bi];
       }
       // pressure: only patch k holds p_k (multiplicity 1) -> output now
       if (t >= 1 && t <= fz::kNOUT && s >= y0 && s < y1) {
@@ -712,9 +756,10 @@ inline int fused_chunk(const LevelGeom& g, int nstrips, int nsm) {
   return (g.N + 1 + chunks - 1) / chunks;
 }
 
-inline int launch_fused_sweep(const LevelGeom& g, double omega, int scalar_w, const FusedFactors& F,
-                              const double* dinv, const double* xin, const double* b, double* xout, int nsm,
-                              cudaStream_t s) {
+inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,
+                              const double* dinv, double* bd, const double* xin, const double* b, double* xout,
+                              int nsm, cudaStream_t s) {
+  k_boundary_patches<<<(unsigned)bd_count(g.N), 64, 0, s>>>(g, nu, dinv, xin, b, bd);
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -725,7 +770,7 @@ inline int launch_fused_sweep(const LevelGeom& g, double omega, int scalar_w, co
   }
   const int ncover = (int)std::max<int64_t>(g.pu / 2, g.pp);
   const int nstrips = (ncover + fz::kNOUT - 1) / fz::kNOUT;
-  FusedArgs A{g, omega, scalar_w, 0, dinv, xin, b, xout};
+  FusedArgs A{g, omega, scalar_w, 0, bd, xin, b, xout};
   A.chunk = fused_chunk(g, nstrips, nsm);
   const dim3 grid(nstrips, (g.N + 1 + A.chunk - 1) / A.chunk);
   if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F);
