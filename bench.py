@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for libsvk.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl svk|reference]
+
+Workload (BASELINE.json configs[2]): 2D Stokes, Q2-Q1 Taylor-Hood on a 4096 x 4096
+structured mesh (151,035,907 DOFs), the paper's manufactured solution
+as synthetic input.  One STEP = one FGMRES solve to 1e-10 right-preconditioned by
+one V(1,1) cycle with additive Vanka relaxation per iteration, which runs
+every row of the hot path: residual, Vanka sweep, restriction, prolongation,
+level-0 solve, V-cycle, FGMRES.  The hierarchy + patch setup (svk_create) runs once
+per context, as the paper precomputes its patch inverses; its time is
+reported as `setup_s`.
+
+value  = DOFs solved per second (whole job: N GPUs x one 4096^2 problem each).
+sweep  = the finest-level Vanka sweeps inside the timed solves (CUDA events on the
+         sweep stream, svk_set_profiling): DOF/s, algorithmic HBM GB/s, roofline.
+e2e    = the same solve through svk_solve_host with pinned HOST buffers (H2D of
+         b and x0, D2H of x inside the timed region).
+--impl reference  times the CPU oracle (oracle/, C++ + OpenMP, fp64) on a bounded
+         sample of the same workload (a 256^2 solve per step) on the host cores.
+Multi-GPU (N > 1, torchrun): until the row-slab layer lands every rank solves its
+own 4096^2 problem (independent replicas, weak scaling, no data-path collective);
+time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Vanka sweep DOF/s + HBM GB/s vs peak; FGMRES-MG time-to-solve at 1/2/4/8 B200"
+# Algorithmic work per pressure node (= per patch) of one fused sweep; see
+# DESIGN.md "Roofline accounting".  Bytes: read x, read b, write x_out = 3 x 8 B
+# per DOF.  FP64 flops of the parity-blocked Schur patch solve + stencil residual.
+FLOPS_PER_NODE = 1314
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: guide's SM count x DFMA/clk x max clock
+L2_BYTES = 126e6
+
+
+def n_dof(N: int) -> int:
+    return 2 * (2 * N + 1) ** 2 + (N + 1) ** 2
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram__bytes_read.sum + write.sum per fused-sweep launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if p[5 + k].lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle on a bounded sample, rank 0 only."""
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return 0
+    import oracle
+    N = args.ref_n
+    o = oracle.Oracle(N)
+    b, x0 = o.problem(oracle.MMS_PAPER)
+    for _ in range(args.warmup):
+        o.fgmres(b, x0, rtol=args.rtol)
+    t = []
+    its = 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, its, _, _, _ = o.fgmres(b, x0, rtol=args.rtol)
+        t.append(time.perf_counter() - t0)
+    tot = sum(t)
+    value = n_dof(N) * args.steps / tot
+    cores = oracle.max_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args),
+        "iterations": its,
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "oracle",
+                         "sample": "FGMRES+V(1,1)-Vanka solve of the %d^2 MMS problem per step (oracle C++/OpenMP, "
+                                   "setup excluded)" % N},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args):
+    return {"workload": "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka"
+                        % (args.n, args.n),
+            "N": args.n, "levels_to": 4, "dofs": n_dof(args.n), "omega_v": 0.8, "weighting": "multiplicity",
+            "sweep_impl": args.sweep, "l2": "inputs exceed L2 (%.2f GB per vector vs 126 MB L2)"
+            % (n_dof(args.n) * 8 / 1e9), "parallelism": "replicas%d" % args.gpus}
+
+
+def cpu_baseline(args):
+    import oracle
+    N = args.cpu_n
+    o = oracle.Oracle(N)
+    b, x0 = o.problem(oracle.MMS_PAPER)
+    t0 = time.perf_counter()
+    _, its, _, _, _ = o.fgmres(b, x0, rtol=args.rtol)
+    t = time.perf_counter() - t0
+    return {"value": n_dof(N) / t, "unit": "DOF/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": "one FGMRES+V(1,1)-Vanka solve of the %d^2 MMS problem to %g (%d iterations, %.1f s; "
+                      "oracle C++/OpenMP, setup excluded)" % (N, args.rtol, its, t)}
+
+
+def run_svk(args):
+    import numpy as np
+    import torch
+    from paper_2401_06277_b200 import Solver
+
+    world, rank, local = dist_setup(args)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    N = args.n
+    t0 = time.perf_counter()
+    S = Solver(N, sweep=args.sweep, device=dev)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    b, x0 = S.set_problem("mms_paper")
+    x = S.new_vector()
+
+    def step():
+        x.copy_(x0)
+        return S.fgmres(b, x, rtol=args.rtol, maxit=200)
+
+    for _ in range(args.warmup):
+        rep, _ = step()
+    S.set_profiling(True)
+    S.sweep_stats()  # reset
+    clocks = ClockSampler(dev)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = S.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = []
+    for _ in range(args.steps):
+        rep, _ = step()
+        reps.append(rep)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = S.launch_count - launches0
+    nsw, sw_ms = S.sweep_stats()
+    S.set_profiling(False)
+    t = e0.elapsed_time(e1) / 1e3
+    if dist:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    ms_step = 1e3 * t / args.steps
+    value = world * n_dof(N) * args.steps / t
+    its = [r["iterations"] for r in reps]
+
+    # sweep roofline (dominant kernel)
+    t_sweep = sw_ms / 1e3 / max(nsw, 1)
+    nodes = (N + 1) ** 2
+    bytes_alg = 3 * 8 * n_dof(N)
+    hbm_peak, hbm_src = measured_peaks()
+    sweep_gbs = bytes_alg / t_sweep / 1e9
+    flops = FLOPS_PER_NODE * nodes
+    achieved_tf = flops / t_sweep / 1e12
+    traffic = ncu_traffic()
+    roofline = {"bound": "alu", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved_tf / FP64_PEAK_TFLOPS,
+                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "kernel": "Vanka sweep (k_boundary_patches + k_vanka_fused), finest level",
+                "launches": nsw, "avg_ms": 1e3 * t_sweep,
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md counts)",
+                "hbm": {"achieved": sweep_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sweep_gbs / hbm_peak,
+                        "peak_source": hbm_src, "algorithmic_bytes": bytes_alg}}
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        bh = S.to_compact(b).cpu().pin_memory()
+        x0h = S.to_compact(x0).cpu().pin_memory()
+        xh = torch.empty_like(bh).pin_memory()
+        bn, x0n, xn = bh.numpy(), x0h.numpy(), xh.numpy()
+        S.solve_host(bn, x0n, rtol=args.rtol, x_host=xn)  # warm
+        if dist:
+            dist.barrier()
+        te = []
+        for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
+            _, repe = S.solve_host(bn, x0n, rtol=args.rtol, x_host=xn)
+            te.append(time.perf_counter() - t1)
+        tmax = sum(te)
+        if dist:
+            tt = torch.tensor([tmax], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tmax = float(tt.item())
+        e2e = {"value": world * n_dof(N) * args.e2e_steps / tmax, "unit": "DOF/s",
+               "h2d_bytes_per_step": 2 * n_dof(N) * 8, "d2h_bytes_per_step": n_dof(N) * 8,
+               "steps": args.e2e_steps, "ms_per_step": 1e3 * tmax / args.e2e_steps,
+               "api": "svk_solve_host (compact host arrays, pinned)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper manufactured solution, P:76-81)",
+            "config": config_dict(args),
+            "time_to_solve_s": ms_step / 1e3, "iterations": its[-1], "iterations_all": its,
+            "rel_residual": reps[-1]["rel_residual"], "setup_s": setup_s,
+            "t_vcycle_s": reps[-1]["t_vcycle_s"], "t_orth_s": reps[-1]["t_orth_s"],
+            "sweep": {"dof_per_s": n_dof(N) / t_sweep, "ms": 1e3 * t_sweep, "hbm_gbs_alg": sweep_gbs,
+                      "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["svk", "reference"], default="svk")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--sweep", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=512)
+    ap.add_argument("--ref-n", type=int, default=256)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_svk(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

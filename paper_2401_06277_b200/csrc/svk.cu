@@ -51,6 +51,10 @@ struct svk_ctx {
   double* d_hx = nullptr;
   cudaEvent_t ev[4]{};
   int64_t launches = 0;
+  // sweep profiling (svk_set_profiling / svk_sweep_stats)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // pool, used in (start, stop) pairs
+  size_t prof_used = 0;
   std::string err;
 };
 
@@ -218,7 +222,27 @@ int op_residual(svk_ctx* ctx, int l, const double* x, const double* b, double* r
   return SVK_OK;
 }
 
+int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero,
+                  cudaStream_t s);
 int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
+  const bool timed = ctx->prof && l == ctx->nlev - 1;
+  if (timed) {
+    while (ctx->prof_ev.size() < ctx->prof_used + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->prof_ev.push_back(e);
+    }
+    CK(cudaEventRecord(ctx->prof_ev[ctx->prof_used], s));
+  }
+  TRY(op_sweep_impl(ctx, l, xin, b, xout, x_zero, s));
+  if (timed) {
+    CK(cudaEventRecord(ctx->prof_ev[ctx->prof_used + 1], s));
+    ctx->prof_used += 2;
+  }
+  return SVK_OK;
+}
+int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero,
+                  cudaStream_t s) {
   const LevelGeom& g = ctx->g[l];
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
@@ -486,6 +510,7 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_hb);
   F(ctx->d_hx);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  for (auto e : ctx->prof_ev) cudaEventDestroy(e);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   delete ctx;
@@ -808,6 +833,27 @@ int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y,
 }
 
 int64_t svk_launch_count(const svk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int svk_set_profiling(svk_ctx* ctx, int32_t enable) {
+  if (!ctx) return SVK_ERR_INVALID;
+  ctx->prof = enable != 0;
+  return SVK_OK;
+}
+
+int svk_sweep_stats(svk_ctx* ctx, int64_t* count, double* total_ms) {
+  if (!ctx || !count || !total_ms) return SVK_ERR_INVALID;
+  CK(cudaDeviceSynchronize());
+  double t = 0.0;
+  for (size_t k = 0; k + 1 < ctx->prof_used; k += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->prof_ev[k], ctx->prof_ev[k + 1]));
+    t += ms;
+  }
+  *count = (int64_t)(ctx->prof_used / 2);
+  *total_ms = t;
+  ctx->prof_used = 0;
+  return SVK_OK;
+}
 
 const char* svk_status_string(int status) {
   switch (status) {

@@ -71,6 +71,8 @@ EXPORTS = {
                                  C.POINTER(Report), C.c_void_p]),
     "svk_patch_inverse": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
     "svk_launch_count": (C.c_int64, [C.c_void_p]),
+    "svk_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+    "svk_sweep_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
     "svk_status_string": (C.c_char_p, [C.c_int]),
     "svk_last_error": (C.c_char_p, [C.c_void_p]),
 }
@@ -268,6 +270,15 @@ class Solver:
         self._chk(self.lib.svk_patch_inverse(self._h, level, cat_x, cat_y, out.ctypes.data_as(C.c_void_p),
                                              C.byref(n)))
         return out[: n.value * n.value].reshape(n.value, n.value).copy()
+
+    def set_profiling(self, on: bool = True):
+        self._chk(self.lib.svk_set_profiling(self._h, 1 if on else 0))
+
+    def sweep_stats(self):
+        """(number of finest-level sweeps, summed device ms) since the last call."""
+        n, t = C.c_int64(), C.c_double()
+        self._chk(self.lib.svk_sweep_stats(self._h, C.byref(n), C.byref(t)))
+        return int(n.value), float(t.value)
 
     @property
     def launch_count(self) -> int:
