@@ -41,7 +41,7 @@ METRIC = "Vanka sweep DOF/s + HBM GB/s vs peak; FGMRES-MG time-to-solve at 1/2/4
 # Algorithmic work per pressure node (= per patch) of one fused sweep; see
 # DESIGN.md "Roofline accounting".  Bytes: read x, read b, write x_out = 3 x 8 B
 # per DOF.  FP64 flops of the parity-blocked Schur patch solve + stencil residual.
-FLOPS_PER_NODE = 1314
+FLOPS_PER_NODE = 1316
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: guide's SM count x DFMA/clk x max clock
 L2_BYTES = 126e6
 
