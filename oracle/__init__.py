@@ -75,6 +75,8 @@ def _load():
             "orc_coarse_solve": (None, [P, P, P]),
             "orc_vcycle": (None, [P, P, P]),
             "orc_fgmres": (I, [P, P, P, D, I, P, P, P]),
+            "orc_sweep_sample": (None, [I, D, D, I, P, P, P, I64, P]),
+            "orc_residual_sample": (None, [I, D, P, P, P, I64, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -95,6 +97,27 @@ def _f64(a) -> np.ndarray:
 
 def max_threads() -> int:
     return int(_load().orc_max_threads())
+
+
+def sweep_sample(N: int, x, b, idx, nu: float = 1.0, omega: float = 0.8, weighting: int = WEIGHT_MULT):
+    """Vanka-sweep output at DOFs `idx` of a level with N elements per side, computed
+    from locally assembled element boxes (no global assembly; usable at 4096^2)."""
+    lib = _load()
+    x, b = _f64(x), _f64(b)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.zeros(len(idx))
+    lib.orc_sweep_sample(N, nu, omega, weighting, _ptr(x), _ptr(b), _ptr(idx), len(idx), _ptr(out))
+    return out
+
+
+def residual_sample(N: int, x, b, idx, nu: float = 1.0):
+    """(b - A x) at DOFs `idx` (0 on Dirichlet rows), from locally assembled boxes."""
+    lib = _load()
+    x, b = _f64(x), _f64(b)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.zeros(len(idx))
+    lib.orc_residual_sample(N, nu, _ptr(x), _ptr(b), _ptr(idx), len(idx), _ptr(out))
+    return out
 
 
 class Oracle:

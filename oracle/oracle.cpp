@@ -853,3 +853,181 @@ int orc_fgmres(void* h, const double* b, double* x, double rtol, int maxit, doub
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------------------
+// Sampled evaluation at full size (no global assembly): for a level with N
+// elements per side, compute the Vanka-sweep output or the residual at a list of
+// DOFs, assembling only the elements around the patches involved.  Same
+// quadrature, same sign and BC readings, same dense LU and the same patch / weight
+// definitions as the global path (a row of the operator is exact whenever all
+// elements adjacent to its DOF are in the box).  x, b are compact full vectors.
+// ----------------------------------------------------------------------------
+namespace {
+struct Box {  // elements [ex0,ex1) x [ey0,ey1) assembled into a dense local matrix
+  int N;
+  std::vector<int64_t> dofs;            // local -> global
+  std::map<int64_t, int> loc;           // global -> local
+  std::vector<double> A;                // dense, row-major
+  int n() const { return (int)dofs.size(); }
+};
+void box_assemble(Box& B, int N, double nu, int ex0, int ex1, int ey0, int ey1) {
+  const double h = 1.0 / N;
+  const int64_t nlat = 2 * (int64_t)N + 1, nv = nlat * nlat, npn = N + 1;
+  ex0 = std::max(ex0, 0); ey0 = std::max(ey0, 0); ex1 = std::min(ex1, N); ey1 = std::min(ey1, N);
+  B.N = N;
+  auto add = [&](int64_t g) {
+    if (!B.loc.count(g)) { B.loc[g] = (int)B.dofs.size(); B.dofs.push_back(g); }
+  };
+  for (int ey = ey0; ey < ey1; ++ey)
+    for (int ex = ex0; ex < ex1; ++ex) {
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          add((2 * ey + b) * nlat + 2 * ex + a);
+          add(nv + (2 * ey + b) * nlat + 2 * ex + a);
+        }
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) add(2 * nv + (int64_t)(ey + d) * npn + ex + c);
+    }
+  const int n = B.n();
+  B.A.assign((size_t)n * n, 0.0);
+  // element matrices exactly as in assemble()
+  double Le[9][9] = {{0}}, Bxe[4][9] = {{0}}, Bye[4][9] = {{0}};
+  for (int qx = 0; qx < 3; ++qx)
+    for (int qy = 0; qy < 3; ++qy) {
+      double t = kGP[qx], s = kGP[qy], w = kGW[qx] * kGW[qy] * h * h;
+      double dx[9], dy[9];
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          dx[b * 3 + a] = dq2(a, t) * q2(b, s) / h;
+          dy[b * 3 + a] = q2(a, t) * dq2(b, s) / h;
+        }
+      for (int m = 0; m < 9; ++m)
+        for (int n2 = 0; n2 < 9; ++n2) Le[m][n2] += nu * w * (dx[m] * dx[n2] + dy[m] * dy[n2]);
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) {
+          double phi = q1(c, t) * q1(d, s);
+          for (int m = 0; m < 9; ++m) {
+            Bxe[d * 2 + c][m] += -w * phi * dx[m];
+            Bye[d * 2 + c][m] += -w * phi * dy[m];
+          }
+        }
+    }
+  for (int ey = ey0; ey < ey1; ++ey)
+    for (int ex = ex0; ex < ex1; ++ex) {
+      int vi[9], pi[4];
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) vi[b * 3 + a] = B.loc[(2 * ey + b) * nlat + 2 * ex + a];
+      int vj[9];
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) vj[b * 3 + a] = B.loc[nv + (2 * ey + b) * nlat + 2 * ex + a];
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) pi[d * 2 + c] = B.loc[2 * nv + (int64_t)(ey + d) * npn + ex + c];
+      for (int m = 0; m < 9; ++m)
+        for (int n2 = 0; n2 < 9; ++n2) {
+          B.A[(size_t)vi[m] * n + vi[n2]] += Le[m][n2];
+          B.A[(size_t)vj[m] * n + vj[n2]] += Le[m][n2];
+        }
+      for (int k = 0; k < 4; ++k)
+        for (int m = 0; m < 9; ++m) {
+          B.A[(size_t)pi[k] * n + vi[m]] += Bxe[k][m];
+          B.A[(size_t)pi[k] * n + vj[m]] += Bye[k][m];
+          B.A[(size_t)vi[m] * n + pi[k]] += Bxe[k][m];
+          B.A[(size_t)vj[m] * n + pi[k]] += Bye[k][m];
+        }
+    }
+}
+bool is_dirichlet(int64_t g, int N) {
+  const int64_t nlat = 2 * (int64_t)N + 1, nv = nlat * nlat;
+  if (g >= 2 * nv) return false;
+  const int64_t q = g % nv, i = q % nlat, j = q / nlat;
+  return i == 0 || j == 0 || i == nlat - 1 || j == nlat - 1;
+}
+// the patch DOF list of node (kx,ky) exactly as in build_patches()
+std::vector<int64_t> patch_dofs(int N, int kx, int ky) {
+  const int64_t nlat = 2 * (int64_t)N + 1, nv = nlat * nlat;
+  std::vector<int64_t> d;
+  for (int comp = 0; comp < 2; ++comp)
+    for (int64_t j = 2 * ky - 2; j <= 2 * ky + 2; ++j)
+      for (int64_t i = 2 * kx - 2; i <= 2 * kx + 2; ++i) {
+        if (i < 0 || j < 0 || i >= nlat || j >= nlat) continue;
+        int64_t g = comp * nv + j * nlat + i;
+        if (!is_dirichlet(g, N)) d.push_back(g);
+      }
+  d.push_back(2 * nv + (int64_t)ky * (N + 1) + kx);
+  return d;
+}
+// patches (kx,ky) whose DOF list contains g
+std::vector<std::pair<int, int>> patches_of(int64_t g, int N) {
+  const int64_t nlat = 2 * (int64_t)N + 1, nv = nlat * nlat;
+  std::vector<std::pair<int, int>> out;
+  if (g >= 2 * nv) {
+    const int64_t q = g - 2 * nv;
+    out.push_back({(int)(q % (N + 1)), (int)(q / (N + 1))});
+    return out;
+  }
+  if (is_dirichlet(g, N)) return out;
+  const int64_t q = g % nv, i = q % nlat, j = q / nlat;
+  // every node k with |2k - lattice index| <= 2 (candidates j/2-1 .. j/2+1)
+  for (int64_t ky = std::max<int64_t>(0, j / 2 - 1); ky <= std::min<int64_t>(N, j / 2 + 1); ++ky)
+    if (std::llabs(2 * ky - j) <= 2)
+      for (int64_t kx = std::max<int64_t>(0, i / 2 - 1); kx <= std::min<int64_t>(N, i / 2 + 1); ++kx)
+        if (std::llabs(2 * kx - i) <= 2) out.push_back({(int)kx, (int)ky});
+  return out;
+}
+// residual of row g from the box (the box must hold all elements adjacent to g)
+double box_residual(const Box& B, int64_t g, const double* x, const double* b) {
+  if (is_dirichlet(g, B.N)) return 0.0;
+  const int n = B.n();
+  const int r = B.loc.at(g);
+  double s = b[g];
+  for (int c = 0; c < n; ++c) s -= B.A[(size_t)r * n + c] * x[B.dofs[c]];
+  return s;
+}
+}  // namespace
+
+extern "C" {
+// out[q] = x_out at DOF idx[q] after one Vanka sweep from x (alg:vk)
+void orc_sweep_sample(int N, double nu, double omega, int weighting, const double* x, const double* b,
+                      const int64_t* idx, int64_t count, double* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < count; ++q) {
+    const int64_t g = idx[q];
+    double acc = 0.0;
+    const auto pats = patches_of(g, N);
+    for (auto [kx, ky] : pats) {
+      Box B;
+      box_assemble(B, N, nu, kx - 2, kx + 2, ky - 2, ky + 2);
+      const std::vector<int64_t> d = patch_dofs(N, kx, ky);
+      const int m = (int)d.size();
+      std::vector<double> Ai((size_t)m * m), rhs(m);
+      for (int r2 = 0; r2 < m; ++r2) {
+        for (int c = 0; c < m; ++c) Ai[(size_t)r2 * m + c] = B.A[(size_t)B.loc.at(d[r2]) * B.n() + B.loc.at(d[c])];
+        rhs[r2] = box_residual(B, d[r2], x, b);
+      }
+      std::vector<int> piv;
+      lu_factor(Ai, piv, m);
+      lu_solve(Ai, piv, m, rhs.data());
+      for (int r2 = 0; r2 < m; ++r2)
+        if (d[r2] == g) acc += rhs[r2];
+    }
+    // W_i = omega diag(1/mult) (reading 6), mult = number of patches holding g
+    double w = pats.empty() ? 0.0 : (weighting == 0 ? omega / (double)pats.size() : omega);
+    out[q] = x[g] + w * acc;
+  }
+}
+// out[q] = (b - A x) at DOF idx[q] (0 on Dirichlet rows)
+void orc_residual_sample(int N, double nu, const double* x, const double* b, const int64_t* idx, int64_t count,
+                         double* out) {
+  const int64_t nlat = 2 * (int64_t)N + 1, nv = nlat * nlat;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t q = 0; q < count; ++q) {
+    const int64_t g = idx[q];
+    int i, j;
+    if (g >= 2 * nv) { i = 2 * (int)((g - 2 * nv) % (N + 1)); j = 2 * (int)((g - 2 * nv) / (N + 1)); }
+    else { i = (int)((g % nv) % nlat); j = (int)((g % nv) / nlat); }
+    Box B;
+    box_assemble(B, N, nu, i / 2 - 1, i / 2 + 1, j / 2 - 1, j / 2 + 1);
+    out[q] = box_residual(B, g, x, b);
+  }
+}
+}  // extern "C"

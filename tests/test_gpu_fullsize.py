@@ -1,0 +1,77 @@
+"""Parity at BASELINE.json's full size (4096^2, configs[2]) in the launch
+configuration bench.py times (fused sweep, default hierarchy): sampled outputs
+the oracle computes one by one from locally assembled element boxes
+(oracle.sweep_sample / residual_sample), plus the closed-form nodal exactness
+of the converged FGMRES solution, which holds at any size."""
+import numpy as np
+import pytest
+
+import oracle
+import svk_inputs
+
+pytestmark = pytest.mark.gpu
+
+N = 4096
+
+
+@pytest.fixture(scope="module")
+def solver(gpu):
+    from paper_2401_06277_b200 import Solver
+    return Solver(N)
+
+
+def structured_samples(Nn):
+    """DOFs at the places a tiled kernel gets wrong: domain edges, strip edges
+    (124-node strips), chunk rows, plus pressure nodes there."""
+    lat = 2 * Nn + 1
+    nv = lat * lat
+    cols = sorted({1, 2, 3, 4, 5, lat - 2, lat - 3, lat - 4, lat - 5, 246, 247, 248, 249, 250, 251, 494, 495, 496, 497})
+    rows = sorted({1, 2, 3, lat - 2, lat - 3, 240, 241, 242, 243, 244, 245, 4000, 4001})
+    out = []
+    for j in rows:
+        for i in cols:
+            out += [j * lat + i, nv + j * lat + i]
+    for ky in (0, 1, 2, 121, 122, Nn - 1, Nn):
+        for kx in (0, 1, 2, 123, 124, 125, Nn - 2, Nn):
+            out.append(2 * nv + ky * (Nn + 1) + kx)
+    return np.array(sorted(set(out)), dtype=np.int64)
+
+
+def test_fullsize_sweep_and_residual_sampled(solver):
+    S = solver
+    x = svk_inputs.random_vector(N, 101)
+    b = svk_inputs.random_vector(N, 102)
+    xd, bd = S.from_compact(x), S.from_compact(b)
+    xg = S.to_compact(S.sweep(S.fine, xd, bd)).cpu().numpy()
+    rg = S.to_compact(S.residual(S.fine, xd, bd)).cpu().numpy()
+    idx = np.union1d(svk_inputs.random_sample_indices(N, 103, 400), structured_samples(N))
+    xo = oracle.sweep_sample(N, x, b, idx)
+    ro = oracle.residual_sample(N, x, b, idx)
+    d_g, d_o = xg[idx] - x[idx], xo - x[idx]
+    assert np.abs(d_g - d_o).max() <= 1e-12 * np.abs(d_o).max()
+    assert np.abs(rg[idx] - ro).max() <= 1e-13 * np.abs(ro).max()
+
+
+def test_fullsize_mms_nodal_exactness(solver):
+    S = solver
+    b, x = S.set_problem("mms_paper")
+    rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=60)
+    assert rep["converged"] == 1 and 17 <= rep["iterations"] <= 21  # oracle: 18-19 for N = 16 ... 1024
+    ux, uy, p = S.planes(x)
+    lat = 2 * N + 1
+    xs = np.arange(lat) / (2 * N)
+    err_u = 0.0
+    for j0 in range(0, lat, 1024):  # row blocks keep host memory small
+        ys = xs[j0:j0 + 1024][:, None]
+        X = xs[None, :]
+        eux = X * (1 - X) * (2 * X - 1) * (6 * ys ** 2 - 6 * ys + 1)
+        euy = ys * (ys - 1) * (2 * ys - 1) * (6 * X ** 2 - 6 * X + 1)
+        err_u = max(err_u, np.abs(ux[j0:j0 + 1024].cpu().numpy() - eux).max(),
+                    np.abs(uy[j0:j0 + 1024].cpu().numpy() - euy).max())
+    ps = np.arange(N + 1) / N
+    PX, PY = np.meshgrid(ps, ps)
+    ep = PX ** 2 - 3 * PY ** 2 + 8.0 / 3.0 * PX * PY
+    pn = p.cpu().numpy()
+    err_p = np.abs((pn - pn.mean()) - (ep - ep.mean())).max()
+    # discretisation is nodally exact; the remaining error is the 1e-10 solver tolerance
+    assert err_u < 1e-8 and err_p < 1e-5, (err_u, err_p)

@@ -342,3 +342,20 @@ def test_iteration_counts_oracle_internal():
         b, x0 = o.problem(oracle.MMS_PAPER)
         its[N] = o.fgmres(b, x0)[1]
     assert its == {16: 18, 32: 19, 64: 19}
+
+
+# ---------------------------------------------------------------- sampled (full-size) oracle
+@pytest.mark.parametrize("N", [4, 8, 16])
+def test_sampled_sweep_and_residual_equal_global_oracle(N):
+    """The local-box evaluation used for full-size parity equals the global oracle."""
+    o = oracle.Oracle(N, n_coarse=4)
+    l = o.fine
+    x = svk_inputs.random_vector(N, 21)
+    b = svk_inputs.random_vector(N, 22)
+    idx = np.arange(o.length(l), dtype=np.int64)
+    xs = o.sweep(l, x, b)
+    rs = o.residual(l, x, b)
+    assert rel(oracle.sweep_sample(N, x, b, idx) - x, xs - x) < 1e-12
+    assert rel(oracle.residual_sample(N, x, b, idx), rs) < 1e-13
+    xs2 = oracle.Oracle(N, weighting=oracle.WEIGHT_SCALAR, omega=0.5).sweep(l, x, b)
+    assert rel(oracle.sweep_sample(N, x, b, idx, omega=0.5, weighting=oracle.WEIGHT_SCALAR) - x, xs2 - x) < 1e-12
