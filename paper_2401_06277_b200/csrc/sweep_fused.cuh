@@ -15,6 +15,8 @@
 // Lw^{-1} is block diagonal with blocks EE 9x9, EO 6x6, OE 6x6, OO 4x4
 // (169 FMA instead of 625), and bx lives only in EO, by only in OE.
 #pragma once
+#include <cuda.h>
+#include <cstring>
 #include "stencil.cuh"
 
 namespace svk {
@@ -252,13 +254,29 @@ __global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu,
 //    strip edge (2 patch columns and 7 lattice columns per 124 node columns).
 // =============================================================================
 namespace fz {
-constexpr int kNT = 128, kNPATCH = 126, kNOUT = 124;
-constexpr int XR = 9, XH = 132;   // x ring: rows, doubles per parity half (columns xc0 .. xc0+263)
-constexpr int PR = 4, PW = 136;   // p ring: rows, columns pc0 .. pc0+135
-constexpr int RR = 6, RH = 128;   // residual ring: rows, doubles per parity half (columns rc0 .. rc0+255)
-constexpr int AR = 6;             // accumulator ring rows (same columns as the residual ring)
-constexpr int kSmemDoubles = XR * 4 * XH + PR * PW + RR * 4 * RH + 2 * RH + AR * 4 * RH;
-constexpr int kSmemBytes = kSmemDoubles * 8;
+// strip geometry: P patches per strip (threads 0..P-1), P-2 owned node columns
+constexpr int kNT = 128, kNPATCH = 124, kNOUT = 122, kWarps = kNT / 32;
+constexpr int W = 256;            // ring row width (doubles): x columns xc0..xc0+255, r/acc/b columns rc0..rc0+255
+constexpr int PWID = 128;         // b_p / r_p row width: node columns from kx0-2
+constexpr int PXW = 136;          // p ring box width: node columns pc0 = kx0-4 .. kx0+131
+constexpr int PXS = 144;          // p ring row stride (TMA smem destinations are 128-byte aligned)
+// (TMA box starts must be 16-byte aligned in the innermost dimension: every
+//  box origin here is an even column)
+constexpr int XPR = 5;            // x ring: row PAIRS (2p+1, 2p+2), each [comp][2 rows][W]
+constexpr int PR = 4;             // p ring rows
+constexpr int BPR = 2;            // b ring row pairs
+constexpr int RR = 5, AR = 5;     // residual / accumulator ring rows, each [comp][W]
+constexpr int OXS = 0;
+constexpr int OPS = OXS + XPR * 4 * W;
+constexpr int OBS = OPS + PR * PXS;
+constexpr int OBP = OBS + BPR * 4 * W;
+constexpr int ORS = OBP + 2 * PWID;
+constexpr int ORP = ORS + RR * 2 * W;
+constexpr int OAS = ORP + 2 * PWID;
+constexpr int OEB = OAS + AR * 2 * W;   // warp-edge buffer [warp][side][row 5][4]
+constexpr int OMB = OEB + kWarps * 2 * 5 * 4;  // 2 mbarriers
+constexpr int kSmemBytes = (OMB + 2) * 8;
+constexpr unsigned kXBytes = 4 * W * 8, kPBytes = PXW * 8, kBBytes = 4 * W * 8, kBPBytes = PWID * 8;
 }  // namespace fz
 
 struct FusedArgs {
@@ -267,193 +285,184 @@ struct FusedArgs {
   int scalar_w;
   int chunk;            // node rows per CTA
   const double* bd;     // boundary-patch corrections (k_boundary_patches), slot-major
-  const double* xin;    // unused when the kernel is instantiated with XZERO
-  const double* b;
   double* xout;
+};
+struct FusedMaps {      // TMA descriptors (host-encoded per launch)
+  CUtensorMap xv;       // x velocity planes: dims {lat, lat, 2}, box {256, 2, 2}
+  CUtensorMap xp;       // x pressure plane:  dims {N+1, N+1},  box {128, 1}
+  CUtensorMap bv;       // b velocity planes
+  CUtensorMap bp;       // b pressure plane
 };
 
 __device__ __forceinline__ int pmod(int a, int m) {
   const int r = a % m;
   return r < 0 ? r + m : r;
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-struct FusedSmem {
-  double* xs;   // [XR][comp][par][XH]
-  double* ps;   // [PR][PW]
-  double* rs;   // [RR][comp][par][RH]
-  double* rps;  // [2][RH]
-  double* as;   // [AR][comp][par][RH]
-  __device__ __forceinline__ double& X(int j, int comp, int par, int q) const {
-    return xs[((pmod(j, fz::XR) * 2 + comp) * 2 + par) * fz::XH + q];
-  }
-  __device__ __forceinline__ double& Pp(int row, int q) const { return ps[(row & 3) * fz::PW + q]; }
-  __device__ __forceinline__ double& R(int j, int comp, int par, int q) const {
-    return rs[((pmod(j, fz::RR) * 2 + comp) * 2 + par) * fz::RH + q];
-  }
-  __device__ __forceinline__ double& RP(int row, int q) const { return rps[(row & 1) * fz::RH + q]; }
-  __device__ __forceinline__ double& Acc(int j, int comp, int par, int q) const {
-    return as[((pmod(j, fz::AR) * 2 + comp) * 2 + par) * fz::RH + q];
-  }
-};
-
-// x lattice row j (both components), columns xc0 .. xc0+263, zero outside the domain
-__device__ __forceinline__ void load_x_row(const FusedSmem& S, const LevelGeom& g, const double* __restrict__ x, int j,
-                                           int xc0) {
-  const bool rowok = j >= 0 && j < g.lat;
-  for (int comp = 0; comp < 2; ++comp) {
-    const double* base = x + (comp ? g.ouy : g.oux);
-    for (int q = threadIdx.x; q < 2 * fz::XH; q += fz::kNT) {
-      const int c = xc0 + q;
-      const bool ok = rowok && c >= 0 && c < g.lat;
-      cp_async8(&S.X(j, comp, q & 1, q >> 1), ok ? base + (int64_t)j * g.pu + c : base, ok);
-    }
-  }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void load_p_row(const FusedSmem& S, const LevelGeom& g, const double* __restrict__ x,
-                                           int row, int pc0) {
-  const bool rowok = row >= 0 && row <= g.N;
-  const double* base = x + g.op;
-  for (int q = threadIdx.x; q < fz::PW; q += fz::kNT) {
-    const int c = pc0 + q;
-    const bool ok = rowok && c >= 0 && c <= g.N;
-    cp_async8(&S.Pp(row & 3, q), ok ? base + (int64_t)row * g.pp + c : base, ok);
-  }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// Residual on lattice rows 2sp+1 (odd) and 2sp+2 (even), lattice columns
-// c0 = rc0 + 2t (even) and c0+1, both components; pressure residual at node
-// (kx0-2+t, sp+1).  Uses x rows 2sp..2sp+4 and p rows sp..sp+2.
+// ring offsets (doubles from the smem base)
+__device__ __forceinline__ int xpair(int p) { return fz::OXS + pmod(p, fz::XPR) * 4 * fz::W; }
+// x lattice row j, component c: pair (j-1)>>1, row-in-pair (j-1)&1, layout [comp][row][W]
+__device__ __forceinline__ int xrow(int j, int c) {
+  return xpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
+}
+__device__ __forceinline__ int prow(int r) { return fz::OPS + (r & 3) * fz::PXS; }
+__device__ __forceinline__ int bpair(int p) { return fz::OBS + (p & 1) * 4 * fz::W; }
+__device__ __forceinline__ int brow(int j, int c) { return bpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W; }
+__device__ __forceinline__ int bprow(int r) { return fz::OBP + (r & 1) * fz::PWID; }
+__device__ __forceinline__ int rrow(int j, int c) { return fz::ORS + pmod(j, fz::RR) * 2 * fz::W + c * fz::W; }
+__device__ __forceinline__ int rprow(int r) { return fz::ORP + (r & 1) * fz::PWID; }
+__device__ __forceinline__ int arow(int j, int c) { return fz::OAS + pmod(j, fz::AR) * 2 * fz::W + c * fz::W; }
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
+
+// Residual on lattice rows 2sp+1 (odd) and 2sp+2 (even) at lattice columns
+// c0 = rc0 + 2t (even) and c0+1, both components, and the pressure residual at
+// node (kx0-2+t, sp+1).  Reads x rows 2sp..2sp+4, p rows sp..sp+2, b rows
+// 2sp+1, 2sp+2 (pair sp), b_p row sp+1.  Each stencil coefficient is loaded once
+// and used for both components; the whole 5x5 windows are loaded first.
 template <bool XZERO>
-__device__ __forceinline__ void fused_residual(const FusedSmem& S, const FusedArgs& A, const FusedFactors& F, int sp,
+__device__ __forceinline__ void fused_residual(double* sm, const FusedArgs& A, const FusedFactors& F, int sp,
                                                int kx0) {
   const LevelGeom& g = A.g;
   const int N = g.N, lat = g.lat, t = threadIdx.x;
-  const int rc0 = 2 * kx0 - 4;
-  const int c0 = rc0 + 2 * t;
+  const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
   const bool c0ok = c0 >= 1 && c0 <= lat - 2, c1ok = c0 + 1 >= 1 && c0 + 1 <= lat - 2;
   const bool j0ok = j0 >= 1 && j0 <= lat - 2, j1ok = j1 >= 1 && j1 <= lat - 2;
-  double ax[2][4];  // [comp][(j0,c0) (j0,c0+1) (j1,c0) (j1,c0+1)]
-  double bu = 0.0;  // B u at the pressure node
   const int na = kx0 - 2 + t, nrow = sp + 1;
   const bool pok = na >= 0 && na <= N && nrow >= 0 && nrow <= N;
-  const bool pint = na >= 1 && na <= N - 1 && nrow >= 1 && nrow <= N - 1;
-  if (!XZERO) {
+  double ax[8];  // (A x) at (j0,c0) (j0,c0+1) (j1,c0) (j1,c0+1) for u_x [0..3] and u_y [4..7]
 #pragma unroll
-    for (int comp = 0; comp < 2; ++comp) {
-      double V[5][5];
+  for (int q = 0; q < 8; ++q) ax[q] = 0.0;
+  double bu = 0.0;
+  if (!XZERO) {
+    double U[5][5], V[5][5];  // window rows 2sp..2sp+4, lattice columns c0-2..c0+2 (x columns 2t..2t+4)
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const double* xu = sm + xrow(2 * sp + r, 0) + 2 * t;
+      const double* xv = sm + xrow(2 * sp + r, 1) + 2 * t;
+      const double2 u01 = lds2(xu), u23 = lds2(xu + 2), v01 = lds2(xv), v23 = lds2(xv + 2);
+      U[r][0] = u01.x; U[r][1] = u01.y; U[r][2] = u23.x; U[r][3] = u23.y; U[r][4] = xu[4];
+      V[r][0] = v01.x; V[r][1] = v01.y; V[r][2] = v23.x; V[r][3] = v23.y; V[r][4] = xv[4];
+    }
+    double Pm[3][3];  // p rows sp..sp+2, nodes kx0-3+t .. kx0-1+t (p ring column node - (kx0-4))
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double* pr = sm + prow(sp + r) + t + 1;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) Pm[r][q] = pr[q];
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      if (r <= 2) {  // odd row j0 sees window rows 0..2 (b = r-1)
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+          const double c = F.L2D[1][0][r + 1][a];
+          ax[0] = fma(c, U[r][a], ax[0]);
+          ax[4] = fma(c, V[r][a], ax[4]);
+        }
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {  // odd column (window column 3): taps 2..4
+          const double c = F.L2D[1][1][r + 1][a];
+          ax[1] = fma(c, U[r][a + 1], ax[1]);
+          ax[5] = fma(c, V[r][a + 1], ax[5]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 5; ++a) {  // even row j1 sees window rows 0..4 (b = r-2)
+        const double c = F.L2D[0][0][r][a];
+        ax[2] = fma(c, U[r][a], ax[2]);
+        ax[6] = fma(c, V[r][a], ax[6]);
+      }
+#pragma unroll
+      for (int a = 1; a < 4; ++a) {
+        const double c = F.L2D[0][1][r][a];
+        ax[3] = fma(c, U[r][a + 1], ax[3]);
+        ax[7] = fma(c, V[r][a + 1], ax[7]);
+      }
+    }
+    const bool pint = na >= 1 && na <= N - 1 && nrow >= 1 && nrow <= N - 1;
+    if (pint) {  // B u on the interior pressure-row pattern (window = U/V)
+#pragma unroll
+      for (int r = 1; r <= 3; ++r) {
+        bu = fma(F.PBX[r][0], U[r][0], bu);
+        bu = fma(F.PBX[r][1], U[r][1], bu);
+        bu = fma(F.PBX[r][3], U[r][3], bu);
+        bu = fma(F.PBX[r][4], U[r][4], bu);
+      }
 #pragma unroll
       for (int r = 0; r < 5; ++r) {
-        const int j = 2 * sp + r;
-        V[r][0] = S.X(j, comp, 0, t);
-        V[r][1] = S.X(j, comp, 1, t);
-        V[r][2] = S.X(j, comp, 0, t + 1);
-        V[r][3] = S.X(j, comp, 1, t + 1);
-        V[r][4] = S.X(j, comp, 0, t + 2);
+        if (r == 2) continue;
+        bu = fma(F.PBY[r][1], V[r][1], bu);
+        bu = fma(F.PBY[r][2], V[r][2], bu);
+        bu = fma(F.PBY[r][3], V[r][3], bu);
       }
-      double l00 = 0, l01 = 0, l10 = 0, l11 = 0;
+    } else if (pok) {  // boundary pressure node: general rows from the class tables
+      const int cx = na == 0 ? 0 : (na == N ? 2 : 1), cy = nrow == 0 ? 0 : (nrow == N ? 2 : 1);
+      double sacc = 0.0;
 #pragma unroll
-      for (int b = -1; b <= 1; ++b) {
+      for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int a = -2; a <= 2; ++a) l00 = fma(F.L2D[1][0][b + 2][a + 2], V[1 + b][2 + a], l00);
-#pragma unroll
-        for (int a = -1; a <= 1; ++a) l01 = fma(F.L2D[1][1][b + 2][a + 2], V[1 + b][3 + a], l01);
-      }
-#pragma unroll
-      for (int b = -2; b <= 2; ++b) {
-#pragma unroll
-        for (int a = -2; a <= 2; ++a) l10 = fma(F.L2D[0][0][b + 2][a + 2], V[2 + b][2 + a], l10);
-#pragma unroll
-        for (int a = -1; a <= 1; ++a) l11 = fma(F.L2D[0][1][b + 2][a + 2], V[2 + b][3 + a], l11);
-      }
-      ax[comp][0] = l00;
-      ax[comp][1] = l01;
-      ax[comp][2] = l10;
-      ax[comp][3] = l11;
-      // B u at node (na, nrow): window rows 2sp..2sp+4 = V rows, columns 2na-2.. = V columns
-      if (pint) {
-        if (comp == 0) {
-#pragma unroll
-          for (int oy = 1; oy <= 3; ++oy) {
-            bu = fma(F.PBX[oy][0], V[oy][0], bu);
-            bu = fma(F.PBX[oy][1], V[oy][1], bu);
-            bu = fma(F.PBX[oy][3], V[oy][3], bu);
-            bu = fma(F.PBX[oy][4], V[oy][4], bu);
-          }
-        } else {
-#pragma unroll
-          for (int oy = 0; oy < 5; ++oy) {
-            if (oy == 2) continue;
-            bu = fma(F.PBY[oy][1], V[oy][1], bu);
-            bu = fma(F.PBY[oy][2], V[oy][2], bu);
-            bu = fma(F.PBY[oy][3], V[oy][3], bu);
-          }
-        }
-      } else if (pok) {  // boundary pressure node: general rows from the class tables
-        const int cx = na == 0 ? 0 : (na == N ? 2 : 1), cy = nrow == 0 ? 0 : (nrow == N ? 2 : 1);
-        double s = 0.0;
-#pragma unroll
-        for (int oy = 0; oy < 5; ++oy)
-#pragma unroll
-          for (int ox = 0; ox < 5; ++ox)
-            s += (comp == 0 ? c_st.CR[cy][oy] * c_st.GR[cx][ox] : c_st.GR[cy][oy] * c_st.CR[cx][ox]) * V[oy][ox];
-        bu = fma(-g.h, s, bu);
-      }
+        for (int ox = 0; ox < 5; ++ox)
+          sacc += c_st.CR[cy][r] * c_st.GR[cx][ox] * U[r][ox] + c_st.GR[cy][r] * c_st.CR[cx][ox] * V[r][ox];
+      bu = -g.h * sacc;
     }
-    // B^T p: p rows sp..sp+2, node columns kx0-3+t .. (p-array q = t .. t+2)
-    double Pm[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int q = 0; q < 3; ++q) Pm[r][q] = S.Pp(sp + r, t + q);
-    // odd row j0 = 2sp+1: nodes ky = sp, sp+1 (ty 0,1); even row j1: ky = sp..sp+2 (ty 0..2)
-    // even column c0: kx = q 0..2 (G col nonzero at 0,2; C^ col nonzero at 1); odd column: q 1..2
-    ax[0][0] += F.GX[1][0][0][0] * Pm[0][0] + F.GX[1][0][0][2] * Pm[0][2] + F.GX[1][0][1][0] * Pm[1][0] +
-                F.GX[1][0][1][2] * Pm[1][2];
-    ax[0][1] += F.GX[1][1][0][0] * Pm[0][1] + F.GX[1][1][0][1] * Pm[0][2] + F.GX[1][1][1][0] * Pm[1][1] +
-                F.GX[1][1][1][1] * Pm[1][2];
-    ax[0][2] += F.GX[0][0][1][0] * Pm[1][0] + F.GX[0][0][1][2] * Pm[1][2];
-    ax[0][3] += F.GX[0][1][1][0] * Pm[1][1] + F.GX[0][1][1][1] * Pm[1][2];
-    ax[1][0] += F.GY[1][0][0][1] * Pm[0][1] + F.GY[1][0][1][1] * Pm[1][1];
-    ax[1][1] += F.GY[1][1][0][0] * Pm[0][1] + F.GY[1][1][0][1] * Pm[0][2] + F.GY[1][1][1][0] * Pm[1][1] +
-                F.GY[1][1][1][1] * Pm[1][2];
-    ax[1][2] += F.GY[0][0][0][1] * Pm[0][1] + F.GY[0][0][2][1] * Pm[2][1];
-    ax[1][3] += F.GY[0][1][0][0] * Pm[0][1] + F.GY[0][1][0][1] * Pm[0][2] + F.GY[0][1][2][0] * Pm[2][1] +
-                F.GY[0][1][2][1] * Pm[2][2];
-  } else {
-#pragma unroll
-    for (int comp = 0; comp < 2; ++comp)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ax[comp][q] = 0.0;
+    ax[0] += F.GX[1][0][0][0] * Pm[0][0] + F.GX[1][0][0][2] * Pm[0][2] + F.GX[1][0][1][0] * Pm[1][0] +
+             F.GX[1][0][1][2] * Pm[1][2];
+    ax[1] += F.GX[1][1][0][0] * Pm[0][1] + F.GX[1][1][0][1] * Pm[0][2] + F.GX[1][1][1][0] * Pm[1][1] +
+             F.GX[1][1][1][1] * Pm[1][2];
+    ax[2] += F.GX[0][0][1][0] * Pm[1][0] + F.GX[0][0][1][2] * Pm[1][2];
+    ax[3] += F.GX[0][1][1][0] * Pm[1][1] + F.GX[0][1][1][1] * Pm[1][2];
+    ax[4] += F.GY[1][0][0][1] * Pm[0][1] + F.GY[1][0][1][1] * Pm[1][1];
+    ax[5] += F.GY[1][1][0][0] * Pm[0][1] + F.GY[1][1][0][1] * Pm[0][2] + F.GY[1][1][1][0] * Pm[1][1] +
+             F.GY[1][1][1][1] * Pm[1][2];
+    ax[6] += F.GY[0][0][0][1] * Pm[0][1] + F.GY[0][0][2][1] * Pm[2][1];
+    ax[7] += F.GY[0][1][0][0] * Pm[0][1] + F.GY[0][1][0][1] * Pm[0][2] + F.GY[0][1][2][0] * Pm[2][1] +
+             F.GY[0][1][2][1] * Pm[2][2];
   }
-  // r = b - A x, masked; store to the residual ring
+  // r = b - A x on non-Dirichlet points (b columns rc0.. = 2t, 2t+1 of the b ring)
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    const double* bb = A.b + (comp ? g.ouy : g.oux);
-    double b00 = 0, b01 = 0, b10 = 0, b11 = 0;
-    if (j0ok && (c0ok || c1ok)) {
-      const double2 v = *reinterpret_cast<const double2*>(bb + (int64_t)j0 * g.pu + c0);
-      b00 = v.x;
-      b01 = v.y;
-    }
-    if (j1ok && (c0ok || c1ok)) {
-      const double2 v = *reinterpret_cast<const double2*>(bb + (int64_t)j1 * g.pu + c0);
-      b10 = v.x;
-      b11 = v.y;
-    }
-    S.R(j0, comp, 0, t) = (j0ok && c0ok) ? b00 - ax[comp][0] : 0.0;
-    S.R(j0, comp, 1, t) = (j0ok && c1ok) ? b01 - ax[comp][1] : 0.0;
-    S.R(j1, comp, 0, t) = (j1ok && c0ok) ? b10 - ax[comp][2] : 0.0;
-    S.R(j1, comp, 1, t) = (j1ok && c1ok) ? b11 - ax[comp][3] : 0.0;
+    const double2 b0 = lds2(sm + brow(j0, comp) + 2 * t), b1 = lds2(sm + brow(j1, comp) + 2 * t);
+    sts2(sm + rrow(j0, comp) + 2 * t, (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0,
+         (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0);
+    sts2(sm + rrow(j1, comp) + 2 * t, (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0,
+         (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0);
   }
-  S.RP(nrow, t) = pok ? A.b[g.op + (int64_t)nrow * g.pp + na] - bu : 0.0;
+  sm[rprow(nrow) + t] = pok ? sm[bprow(nrow) + t] - bu : 0.0;
 }
 
 // forward even/odd transform of one 5-vector with stride st (in place)
@@ -489,252 +498,305 @@ __device__ __forceinline__ void inv_transform(double (&v)[25]) {
 #pragma unroll
   for (int r = 0; r < 5; ++r) SVK_UNSPLIT5(v, r * 5, 1);
 }
-// yhat = B rhat, block by block, in place (transformed index ty*5+tx)
-__device__ __forceinline__ void apply_blocks(double (&v)[25], const FusedFactors& F) {
-  {  // EE: ty,tx in {0,1,2}
-    double in[9], out[9];
+// yhat = B rhat for both components at once: every coefficient is loaded once
+// and feeds two FMAs; all rows of a block accumulate in parallel (ILP).
+template <int NB>
+__device__ __forceinline__ void block_mv2(double (&vx)[25], double (&vy)[25], const double (&B)[NB][NB],
+                                          const int (&pos)[NB]) {
+  double sx[NB], sy[NB];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) in[q] = v[(q / 3) * 5 + q % 3];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) s = fma(F.bee[r][q], in[q], s);
-      out[r] = s;
-    }
-#pragma unroll
-    for (int q = 0; q < 9; ++q) v[(q / 3) * 5 + q % 3] = out[q];
+  for (int r = 0; r < NB; ++r) {
+    sx[r] = 0.0;
+    sy[r] = 0.0;
   }
-  {  // EO: ty in {0,1,2}, tx in {3,4}
-    double in[6], out[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) in[q] = v[(q / 2) * 5 + 3 + q % 2];
+  for (int q = 0; q < NB; ++q) {
+    const double ix = vx[pos[q]], iy = vy[pos[q]];
 #pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) s = fma(F.beo[r][q], in[q], s);
-      out[r] = s;
+    for (int r = 0; r < NB; ++r) {
+      const double c = B[r][q];
+      sx[r] = fma(c, ix, sx[r]);
+      sy[r] = fma(c, iy, sy[r]);
     }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) v[(q / 2) * 5 + 3 + q % 2] = out[q];
   }
-  {  // OE: ty in {3,4}, tx in {0,1,2}
-    double in[6], out[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) in[q] = v[(3 + q / 3) * 5 + q % 3];
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) s = fma(F.boe[r][q], in[q], s);
-      out[r] = s;
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) v[(3 + q / 3) * 5 + q % 3] = out[q];
-  }
-  {  // OO
-    double in[4], out[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) in[q] = v[(3 + q / 2) * 5 + 3 + q % 2];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s = fma(F.boo[r][q], in[q], s);
-      out[r] = s;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[(3 + q / 2) * 5 + 3 + q % 2] = out[q];
+  for (int r = 0; r < NB; ++r) {
+    vx[pos[r]] = sx[r];
+    vy[pos[r]] = sy[r];
   }
 }
 
 // Generic patch: (vx, vy, rp) = patch residual in; (vx, vy) = (du, dv) out; returns dp.
 __device__ __forceinline__ double solve_generic(double (&vx)[25], double (&vy)[25], double rp, const FusedFactors& F) {
+  constexpr int pee[9] = {0, 1, 2, 5, 6, 7, 10, 11, 12};
+  constexpr int peo[6] = {3, 4, 8, 9, 13, 14};
+  constexpr int poe[6] = {15, 16, 17, 20, 21, 22};
+  constexpr int poo[4] = {18, 19, 23, 24};
   fwd_transform(vx);
   fwd_transform(vy);
   double sx = 0.0, sy = 0.0;
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
-    sx = fma(F.chx[q], vx[(q / 2) * 5 + 3 + q % 2], sx);
-    sy = fma(F.chy[q], vy[(3 + q / 3) * 5 + q % 3], sy);
+    sx = fma(F.chx[q], vx[peo[q]], sx);
+    sy = fma(F.chy[q], vy[poe[q]], sy);
   }
   const double dp = (sx + sy - rp) * F.inv_sigma;
-  apply_blocks(vx, F);
-  apply_blocks(vy, F);
+  block_mv2<9>(vx, vy, F.bee, pee);
+  block_mv2<6>(vx, vy, F.beo, peo);
+  block_mv2<6>(vx, vy, F.boe, poe);
+  block_mv2<4>(vx, vy, F.boo, poo);
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
-    vx[(q / 2) * 5 + 3 + q % 2] = fma(-F.cpx[q], dp, vx[(q / 2) * 5 + 3 + q % 2]);
-    vy[(3 + q / 3) * 5 + q % 3] = fma(-F.cpy[q], dp, vy[(3 + q / 3) * 5 + q % 3]);
+    vx[peo[q]] = fma(-F.cpx[q], dp, vx[peo[q]]);
+    vy[poe[q]] = fma(-F.cpy[q], dp, vy[poe[q]]);
   }
   inv_transform(vx);
   inv_transform(vy);
   return dp;
 }
 
+// issue the TMA loads a step needs (one elected thread): x row pair p (rows 2p+1,
+// 2p+2) both components, p row pr, b row pair pb, b_p row rbp
 template <bool XZERO>
-__global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F) {
-  extern __shared__ double smem[];
-  FusedSmem S;
-  S.xs = smem;
-  S.ps = S.xs + fz::XR * 4 * fz::XH;
-  S.rs = S.ps + fz::PR * fz::PW;
-  S.rps = S.rs + fz::RR * 4 * fz::RH;
-  S.as = S.rps + 2 * fz::RH;
+__device__ __forceinline__ void issue_loads(double* sm, const FusedMaps& M, uint64_t* bar, int xc0, int pc0, int kx0,
+                                            int xp, int pr, int pb, int rbp, bool with_x, bool with_b) {
+  unsigned bytes = 0;
+  if (!XZERO && with_x) bytes += fz::kXBytes + fz::kPBytes;
+  if (with_b) bytes += fz::kBBytes + fz::kBPBytes;
+  mbar_expect_tx(bar, bytes);
+  if (!XZERO && with_x) {
+    tma_load_3d(sm + xpair(xp), &M.xv, xc0, 2 * xp + 1, 0, bar);
+    tma_load_2d(sm + prow(pr), &M.xp, pc0, pr, bar);
+  }
+  if (with_b) {
+    tma_load_3d(sm + bpair(pb), &M.bv, xc0 + 2, 2 * pb + 1, 0, bar);
+    tma_load_2d(sm + bprow(rbp), &M.bp, kx0 - 2, rbp, bar);
+  }
+}
+
+template <bool XZERO>
+__global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F,
+                                                            const __grid_constant__ FusedMaps M) {
+  extern __shared__ __align__(1024) double sm[];
   const LevelGeom& g = A.g;
   const int N = g.N, lat = g.lat;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int kx0 = blockIdx.x * fz::kNOUT;
   const int y0 = blockIdx.y * A.chunk;
   const int y1 = min(y0 + A.chunk, N + 1);
   if (y0 >= y1) return;
-  const int xc0 = 2 * kx0 - 6, pc0 = kx0 - 3;
+  const int xc0 = 2 * kx0 - 6, pc0 = kx0 - 4;
   const int sB = y0 - 1, sE = y1;
-  const double* xin = A.xin;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + fz::OMB);
+  unsigned phase[2] = {0u, 0u};
 
-  for (int q = t; q < fz::AR * 4 * fz::RH; q += fz::kNT) S.as[q] = 0.0;
-  if (!XZERO) {
-    for (int j = 2 * sB - 4; j <= 2 * sB + 4; ++j) load_x_row(S, g, xin, j, xc0);
-    for (int r = sB - 2; r <= sB + 1; ++r) load_p_row(S, g, xin, r, pc0);
-    cp_commit();
-    cp_wait_all();
+  for (int q = t; q < fz::AR * 2 * fz::W; q += fz::kNT) sm[fz::OAS + q] = 0.0;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  fused_residual<XZERO>(S, A, F, sB - 2, kx0);
-  fused_residual<XZERO>(S, A, F, sB - 1, kx0);
-  __syncthreads();
-  if (!XZERO) {
-    load_p_row(S, g, xin, sB + 2, pc0);
-    cp_commit();
-    cp_wait_all();
+  // prologue: x pairs sB-3 .. sB+1 (rows 2sB-5 .. 2sB+4), p rows sB-2 .. sB+1,
+  // b pairs sB-2, sB-1 (rows 2sB-3 .. 2sB), b_p rows sB-1, sB  -> barrier 0
+  if (t == 0) {
+    unsigned bytes = 2 * fz::kBBytes + 2 * fz::kBPBytes + (XZERO ? 0u : 5 * fz::kXBytes + 4 * fz::kPBytes);
+    mbar_expect_tx(&bars[0], bytes);
+    if (!XZERO) {
+      for (int p = sB - 3; p <= sB + 1; ++p) tma_load_3d(sm + xpair(p), &M.xv, xc0, 2 * p + 1, 0, &bars[0]);
+      for (int r = sB - 2; r <= sB + 1; ++r) tma_load_2d(sm + prow(r), &M.xp, pc0, r, &bars[0]);
+    }
+    for (int p = sB - 2; p <= sB - 1; ++p) tma_load_3d(sm + bpair(p), &M.bv, xc0 + 2, 2 * p + 1, 0, &bars[0]);
+    for (int r = sB - 1; r <= sB; ++r) tma_load_2d(sm + bprow(r), &M.bp, kx0 - 2, r, &bars[0]);
   }
+  mbar_wait(&bars[0], phase[0]);
+  phase[0] ^= 1u;
+  fused_residual<XZERO>(sm, A, F, sB - 2, kx0);
+  fused_residual<XZERO>(sm, A, F, sB - 1, kx0);
   __syncthreads();
+  // data of step sB: p row sB+2, b pair sB, b_p row sB+1 -> barrier 1
+  if (t == 0) {
+    unsigned bytes = fz::kBBytes + fz::kBPBytes + (XZERO ? 0u : fz::kPBytes);
+    mbar_expect_tx(&bars[1], bytes);
+    if (!XZERO) tma_load_2d(sm + prow(sB + 2), &M.xp, pc0, sB + 2, &bars[1]);
+    tma_load_3d(sm + bpair(sB), &M.bv, xc0 + 2, 2 * sB + 1, 0, &bars[1]);
+    tma_load_2d(sm + bprow(sB + 1), &M.bp, kx0 - 2, sB + 1, &bars[1]);
+  }
+  mbar_wait(&bars[1], phase[1]);
+  phase[1] ^= 1u;
 
   const int kxp = kx0 - 1 + t;  // this thread's patch column
+  double* eb = sm + fz::OEB;
   for (int s = sB; s <= sE; ++s) {
-    if (!XZERO) {
-      load_x_row(S, g, xin, 2 * s + 5, xc0);
-      load_x_row(S, g, xin, 2 * s + 6, xc0);
-      load_p_row(S, g, xin, s + 3, pc0);
-      cp_commit();
+    // prefetch the data of step s+1: x pair s+2 (rows 2s+5, 2s+6), p row s+3,
+    // b pair s+1 (rows 2s+3, 2s+4), b_p row s+2
+    uint64_t* nbar = &bars[(s - sB) & 1];
+    if (t == 0) {
+      unsigned bytes = fz::kBBytes + fz::kBPBytes + (XZERO ? 0u : fz::kXBytes + fz::kPBytes);
+      mbar_expect_tx(nbar, bytes);
+      if (!XZERO) {
+        tma_load_3d(sm + xpair(s + 2), &M.xv, xc0, 2 * s + 5, 0, nbar);
+        tma_load_2d(sm + prow(s + 3), &M.xp, pc0, s + 3, nbar);
+      }
+      tma_load_3d(sm + bpair(s + 1), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
+      tma_load_2d(sm + bprow(s + 2), &M.bp, kx0 - 2, s + 2, nbar);
     }
-    fused_residual<XZERO>(S, A, F, s, kx0);
+    fused_residual<XZERO>(sm, A, F, s, kx0);
     __syncthreads();
 
     // ---- patch solve (alg:vk line 2: A_i delta_i = V_i r, exactly) ----
     double vx[25], vy[25];
     double dp = 0.0;
     const bool valid = t < fz::kNPATCH && kxp >= 0 && kxp <= N && s >= 0 && s <= N;
-    if (valid) {
+    const bool generic = kxp >= 2 && kxp <= N - 2 && s >= 2 && s <= N - 2;
+    if (valid && generic) {
 #pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        const int j = 2 * s - 2 + oy;
-        vx[oy * 5 + 0] = S.R(j, 0, 0, t);
-        vx[oy * 5 + 1] = S.R(j, 0, 1, t);
-        vx[oy * 5 + 2] = S.R(j, 0, 0, t + 1);
-        vx[oy * 5 + 3] = S.R(j, 0, 1, t + 1);
-        vx[oy * 5 + 4] = S.R(j, 0, 0, t + 2);
-        vy[oy * 5 + 0] = S.R(j, 1, 0, t);
-        vy[oy * 5 + 1] = S.R(j, 1, 1, t);
-        vy[oy * 5 + 2] = S.R(j, 1, 0, t + 1);
-        vy[oy * 5 + 3] = S.R(j, 1, 1, t + 1);
-        vy[oy * 5 + 4] = S.R(j, 1, 0, t + 2);
+      for (int oy = 0; oy < 5; ++oy) {  // window columns 2kxp-2.. = ring columns 2t .. 2t+4
+        const double* ru = sm + rrow(2 * s - 2 + oy, 0) + 2 * t;
+        const double* rv = sm + rrow(2 * s - 2 + oy, 1) + 2 * t;
+        const double2 u01 = lds2(ru), u23 = lds2(ru + 2), v01 = lds2(rv), v23 = lds2(rv + 2);
+        vx[oy * 5 + 0] = u01.x; vx[oy * 5 + 1] = u01.y; vx[oy * 5 + 2] = u23.x; vx[oy * 5 + 3] = u23.y;
+        vx[oy * 5 + 4] = ru[4];
+        vy[oy * 5 + 0] = v01.x; vy[oy * 5 + 1] = v01.y; vy[oy * 5 + 2] = v23.x; vy[oy * 5 + 3] = v23.y;
+        vy[oy * 5 + 4] = rv[4];
       }
-      const double rp = S.RP(s, t + 1);
-      if (kxp >= 2 && kxp <= N - 2 && s >= 2 && s <= N - 2) {
-        dp = solve_generic(vx, vy, rp, F);
-      } else {  // precomputed by k_boundary_patches
-        const int64_t nb = bd_count(N), bi = bd_index(kxp, s, N);
+      dp = solve_generic(vx, vy, sm[rprow(s) + t + 1], F);
+    } else if (valid) {  // precomputed by k_boundary_patches
+      const int64_t nb = bd_count(N), bi = bd_index(kxp, s, N);
 #pragma unroll
-        for (int q = 0; q < 25; ++q) {
-          vx[q] = A.bd[q * nb + bi];
-          vy[q] = A.bd[(25 + q) * nb + bi];
-        }
-        dp = A.bd[50 * nb + bi];
+      for (int q = 0; q < 25; ++q) {
+        vx[q] = A.bd[q * nb + bi];
+        vy[q] = A.bd[(25 + q) * nb + bi];
       }
-      // pressure: only patch k holds p_k (multiplicity 1) -> output now
-      if (t >= 1 && t <= fz::kNOUT && s >= y0 && s < y1) {
-        const double xp = XZERO ? 0.0 : S.Pp(s, t + 2);
-        A.xout[g.op + (int64_t)s * g.pp + kxp] = fma(A.omega, dp, xp);
+      dp = A.bd[50 * nb + bi];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 25; ++q) {
+        vx[q] = 0.0;
+        vy[q] = 0.0;
       }
-    } else if (t >= 1 && t <= fz::kNOUT && s >= y0 && s < y1 && kxp > N && kxp < g.pp) {
-      A.xout[g.op + (int64_t)s * g.pp + kxp] = 0.0;  // pitch padding
     }
-    // ---- accumulate sum_i V_i^T delta_i: three conflict-free phases ----
-    if (valid) {
+    // pressure: only patch k holds p_k (multiplicity 1) -> output now
+    if (t >= 1 && t <= fz::kNOUT && s >= y0 && s < y1 && kxp < g.pp) {
+      const double xp = XZERO ? 0.0 : sm[prow(s) + t + 3];
+      A.xout[g.op + (int64_t)s * g.pp + kxp] = kxp <= N ? fma(A.omega, dp, xp) : 0.0;
+    }
+    // ---- accumulate sum_i V_i^T delta_i --------------------------------
+    // patch t's window column ox is ring column 2t+ox.  Warp-local phases
+    // (own columns 2t+2,2t+3; left neighbour's 2t,2t+1; right neighbour's
+    // 2t+4); the two writes that cross a warp boundary go to the edge buffer
+    // and are folded in by their owner after the barrier (deterministic).
+    {
+      double2 a[2][5];
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) a[c][oy] = lds2(sm + arow(2 * s - 2 + oy, c) + 2 * t + 2);
 #pragma unroll
       for (int oy = 0; oy < 5; ++oy) {
-        const int j = 2 * s - 2 + oy;
-        S.Acc(j, 0, 0, t + 1) += vx[oy * 5 + 2];
-        S.Acc(j, 0, 1, t + 1) += vx[oy * 5 + 3];
-        S.Acc(j, 1, 0, t + 1) += vy[oy * 5 + 2];
-        S.Acc(j, 1, 1, t + 1) += vy[oy * 5 + 3];
+        sts2(sm + arow(2 * s - 2 + oy, 0) + 2 * t + 2, a[0][oy].x + vx[oy * 5 + 2], a[0][oy].y + vx[oy * 5 + 3]);
+        sts2(sm + arow(2 * s - 2 + oy, 1) + 2 * t + 2, a[1][oy].x + vy[oy * 5 + 2], a[1][oy].y + vy[oy * 5 + 3]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        double* e = eb + ((warp * 2 + 0) * 5 + oy) * 4;
+        e[0] = vx[oy * 5 + 0];
+        e[1] = vx[oy * 5 + 1];
+        e[2] = vy[oy * 5 + 0];
+        e[3] = vy[oy * 5 + 1];
+      }
+    } else {
+      double2 a[2][5];
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) a[c][oy] = lds2(sm + arow(2 * s - 2 + oy, c) + 2 * t);
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        sts2(sm + arow(2 * s - 2 + oy, 0) + 2 * t, a[0][oy].x + vx[oy * 5 + 0], a[0][oy].y + vx[oy * 5 + 1]);
+        sts2(sm + arow(2 * s - 2 + oy, 1) + 2 * t, a[1][oy].x + vy[oy * 5 + 0], a[1][oy].y + vy[oy * 5 + 1]);
+      }
+    }
+    __syncwarp();
+    if (lane == 31) {
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        double* e = eb + ((warp * 2 + 1) * 5 + oy) * 4;
+        e[0] = vx[oy * 5 + 4];
+        e[2] = vy[oy * 5 + 4];
+      }
+    } else {
+      double a[2][5];
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) a[c][oy] = sm[arow(2 * s - 2 + oy, c) + 2 * t + 4];
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        sm[arow(2 * s - 2 + oy, 0) + 2 * t + 4] = a[0][oy] + vx[oy * 5 + 4];
+        sm[arow(2 * s - 2 + oy, 1) + 2 * t + 4] = a[1][oy] + vy[oy * 5 + 4];
       }
     }
     __syncthreads();
-    if (valid) {
+    if (lane == 31 && warp + 1 < fz::kWarps) {  // left part sent by the next warp's lane 0
 #pragma unroll
       for (int oy = 0; oy < 5; ++oy) {
-        const int j = 2 * s - 2 + oy;
-        S.Acc(j, 0, 0, t) += vx[oy * 5 + 0];
-        S.Acc(j, 0, 1, t) += vx[oy * 5 + 1];
-        S.Acc(j, 1, 0, t) += vy[oy * 5 + 0];
-        S.Acc(j, 1, 1, t) += vy[oy * 5 + 1];
+        const double* e = eb + (((warp + 1) * 2 + 0) * 5 + oy) * 4;
+        double* au = sm + arow(2 * s - 2 + oy, 0) + 2 * t + 2;
+        double* av = sm + arow(2 * s - 2 + oy, 1) + 2 * t + 2;
+        au[0] += e[0];
+        au[1] += e[1];
+        av[0] += e[2];
+        av[1] += e[3];
       }
     }
-    __syncthreads();
-    if (valid) {
+    if (lane == 0 && warp > 0) {  // right part sent by the previous warp's lane 31
 #pragma unroll
       for (int oy = 0; oy < 5; ++oy) {
-        const int j = 2 * s - 2 + oy;
-        S.Acc(j, 0, 0, t + 2) += vx[oy * 5 + 4];
-        S.Acc(j, 1, 0, t + 2) += vy[oy * 5 + 4];
+        const double* e = eb + (((warp - 1) * 2 + 1) * 5 + oy) * 4;
+        sm[arow(2 * s - 2 + oy, 0) + 2 * t + 2] += e[0];
+        sm[arow(2 * s - 2 + oy, 1) + 2 * t + 2] += e[2];
       }
     }
-    __syncthreads();
 
     // ---- lattice rows 2s-2, 2s-1 (node row s-1) are complete ----
+    // thread t owns node column kxp: lattice columns 2kxp, 2kxp+1 = ring columns 2t+2, 2t+3
     const int ny = s - 1;
-    if (t < fz::kNOUT) {
-      const int kx = kx0 + t;
-      const bool rowout = ny >= y0 && ny < y1 && 2 * kx < g.pu;
+    if (t >= 1 && t <= fz::kNOUT && ny >= y0 && ny < y1 && 2 * kxp < g.pu) {
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int j = 2 * ny + rr;
+        if (j > lat - 1) continue;
+        const int i0 = 2 * kxp;
+        const bool jin = j >= 1 && j <= lat - 2;
+        // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
+        const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
+        const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
+        const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
+        const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
 #pragma unroll
         for (int comp = 0; comp < 2; ++comp) {
-          const double a0 = S.Acc(j, comp, 0, t + 2), a1 = S.Acc(j, comp, 1, t + 2);
-          S.Acc(j, comp, 0, t + 2) = 0.0;
-          S.Acc(j, comp, 1, t + 2) = 0.0;
-          if (!rowout || j > lat - 1) continue;
-          const int i0 = 2 * kx;
-          const double x0 = XZERO ? 0.0 : S.X(j, comp, 0, t + 3), x1 = XZERO ? 0.0 : S.X(j, comp, 1, t + 3);
-          const bool jin = j >= 1 && j <= lat - 2;
-          double o0, o1;
-          if (A.scalar_w) {
-            o0 = (jin && i0 >= 1 && i0 <= lat - 2) ? fma(A.omega, a0, x0) : (i0 <= lat - 1 ? x0 : 0.0);
-            o1 = (jin && i0 + 1 <= lat - 2) ? fma(A.omega, a1, x1) : (i0 + 1 <= lat - 1 ? x1 : 0.0);
-          } else {
-            const double wy = (j & 1) ? 0.5 : (1.0 / 3.0);  // 1 / (patches per axis holding the point)
-            o0 = (jin && i0 >= 1 && i0 <= lat - 2) ? fma(A.omega * wy * (1.0 / 3.0), a0, x0) : (i0 <= lat - 1 ? x0 : 0.0);
-            o1 = (jin && i0 + 1 <= lat - 2) ? fma(A.omega * wy * 0.5, a1, x1) : (i0 + 1 <= lat - 1 ? x1 : 0.0);
-          }
-          *reinterpret_cast<double2*>(A.xout + (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) = make_double2(o0, o1);
+          const double2 a = lds2(sm + arow(j, comp) + 2 * t + 2);
+          const double2 x = XZERO ? make_double2(0.0, 0.0) : lds2(sm + xrow(j, comp) + 2 * t + 4);
+          const double o0 = in0 ? fma(w0, a.x, x.x) : (i0 <= lat - 1 ? x.x : 0.0);
+          const double o1 = in1 ? fma(w1, a.y, x.y) : (i0 + 1 <= lat - 1 ? x.y : 0.0);
+          *reinterpret_cast<double2*>(A.xout + (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
+              make_double2(o0, o1);
         }
       }
-    } else {  // ghost accumulator columns nobody outputs: keep them clean
-      const int q = t - fz::kNOUT;  // 0..3 -> columns 0,1 and 126,127 of the ring
-      const int col = q < 2 ? q : fz::kNPATCH + (q - 2);
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int comp = 0; comp < 2; ++comp) {
-          S.Acc(2 * ny + rr, comp, 0, col) = 0.0;
-          S.Acc(2 * ny + rr, comp, 1, col) = 0.0;
-        }
     }
-    if (!XZERO) cp_wait_all();
+    mbar_wait(nbar, phase[(s - sB) & 1]);
+    phase[(s - sB) & 1] ^= 1u;
     __syncthreads();
+    // clear the two finished accumulator rows for reuse
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      sts2(sm + arow(2 * ny, c) + 2 * t, 0.0, 0.0);
+      sts2(sm + arow(2 * ny + 1, c) + 2 * t, 0.0, 0.0);
+    }
   }
 }
 
@@ -756,6 +818,46 @@ inline int fused_chunk(const LevelGeom& g, int nstrips, int nsm) {
   return (g.N + 1 + chunks - 1) / chunks;
 }
 
+// ---- host: TMA descriptors --------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+// velocity planes of a vector: dims {lat cols, lat rows, 2 comps}; box {256, 2, 2}
+inline bool make_vel_map(CUtensorMap* m, const LevelGeom& g, const double* v) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.lat, (cuuint64_t)g.lat, 2};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pu * 8, (cuuint64_t)(g.ouy - g.oux) * 8};
+  const cuuint32_t box[3] = {fz::W, 2, 2};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(v + g.oux), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// pressure plane: dims {N+1, N+1}; box {boxw, 1}
+inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsigned boxw) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)(g.N + 1), (cuuint64_t)(g.N + 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)g.pp * 8};
+  const cuuint32_t box[2] = {boxw, 1};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)(v + g.op), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,
                               const double* dinv, double* bd, const double* xin, const double* b, double* xout,
                               int nsm, cudaStream_t s) {
@@ -770,11 +872,15 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   }
   const int ncover = (int)std::max<int64_t>(g.pu / 2, g.pp);
   const int nstrips = (ncover + fz::kNOUT - 1) / fz::kNOUT;
-  FusedArgs A{g, omega, scalar_w, 0, bd, xin, b, xout};
+  FusedArgs A{g, omega, scalar_w, 0, bd, xout};
   A.chunk = fused_chunk(g, nstrips, nsm);
+  FusedMaps M;
+  std::memset(&M, 0, sizeof(M));
+  if (!make_vel_map(&M.bv, g, b) || !make_p_map(&M.bp, g, b, fz::PWID)) return -2;
+  if (xin && (!make_vel_map(&M.xv, g, xin) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
   const dim3 grid(nstrips, (g.N + 1 + A.chunk - 1) / A.chunk);
-  if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F);
-  else k_vanka_fused<true><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F);
+  if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
+  else k_vanka_fused<true><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
   return 0;
 }
 
