@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu,
 //   x_out = x_in + W sum_i V_i^T A_i^{-1} V_i (b - A x_in)
 //
 // Layout of the work ("owner computes", no atomics, deterministic):
-//  * a CTA of kNT = 128 threads owns a STRIP of kNOUT = 124 node columns
+//  * a CTA of kNT = 128 threads owns a STRIP of kNOUT = 120 node columns
 //    [kx0, kx0+124) and a CHUNK of node rows [y0, y1); it streams upward
 //    through the chunk one node row (= one patch row = two lattice rows) per
 //    step, keeping rings of rows in shared memory:
@@ -254,27 +254,29 @@ __global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu,
 //    strip edge (2 patch columns and 7 lattice columns per 124 node columns).
 // =============================================================================
 namespace fz {
-// strip geometry: P patches per strip (threads 0..P-1), P-2 owned node columns
-constexpr int kNT = 128, kNPATCH = 124, kNOUT = 122, kWarps = kNT / 32;
-constexpr int W = 256;            // ring row width (doubles): x columns xc0..xc0+255, r/acc/b columns rc0..rc0+255
+// strip geometry: 4 warps x 32 patch columns; warp w covers patches 30w .. 30w+31
+// of the strip and owns the middle 30 (lanes 0 and 31 are ghosts), so warps
+// accumulate independently.  Strip = 122 distinct patches, 120 owned node columns.
+constexpr int kNT = 128, kWarps = kNT / 32, kOWN = 30, kNOUT = kWarps * kOWN;
+constexpr int W = 256;            // ring row width (doubles): x columns xc0..xc0+255, r/b columns rc0..rc0+255
 constexpr int PWID = 128;         // b_p / r_p row width: node columns from kx0-2
 constexpr int PXW = 136;          // p ring box width: node columns pc0 = kx0-4 .. kx0+131
 constexpr int PXS = 144;          // p ring row stride (TMA smem destinations are 128-byte aligned)
 // (TMA box starts must be 16-byte aligned in the innermost dimension: every
-//  box origin here is an even column)
-constexpr int XPR = 5;            // x ring: row PAIRS (2p+1, 2p+2), each [comp][2 rows][W]
-constexpr int PR = 4;             // p ring rows
+//  box origin here is an even column.)  Ring depths let warps drift up to one
+//  step apart with a single barrier per step (see the WAR notes in the kernel).
+constexpr int XPR = 6;            // x ring: row PAIRS (2p+1, 2p+2), each [comp][2 rows][W]
+constexpr int PR = 8;             // p ring rows
 constexpr int BPR = 2;            // b ring row pairs
-constexpr int RR = 5, AR = 5;     // residual / accumulator ring rows, each [comp][W]
+constexpr int RR = 7;             // residual ring rows, each [comp][W]
+constexpr int RPR = 4;            // pressure-residual ring rows
 constexpr int OXS = 0;
 constexpr int OPS = OXS + XPR * 4 * W;
 constexpr int OBS = OPS + PR * PXS;
 constexpr int OBP = OBS + BPR * 4 * W;
 constexpr int ORS = OBP + 2 * PWID;
 constexpr int ORP = ORS + RR * 2 * W;
-constexpr int OAS = ORP + 2 * PWID;
-constexpr int OEB = OAS + AR * 2 * W;   // warp-edge buffer [warp][side][row 5][4]
-constexpr int OMB = OEB + kWarps * 2 * 5 * 4;  // 2 mbarriers
+constexpr int OMB = ORP + RPR * PWID;  // 2 mbarriers
 constexpr int kSmemBytes = (OMB + 2) * 8;
 constexpr unsigned kXBytes = 4 * W * 8, kPBytes = PXW * 8, kBBytes = 4 * W * 8, kBPBytes = PWID * 8;
 }  // namespace fz
@@ -337,13 +339,12 @@ __device__ __forceinline__ int xpair(int p) { return fz::OXS + pmod(p, fz::XPR) 
 __device__ __forceinline__ int xrow(int j, int c) {
   return xpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
 }
-__device__ __forceinline__ int prow(int r) { return fz::OPS + (r & 3) * fz::PXS; }
+__device__ __forceinline__ int prow(int r) { return fz::OPS + (r & 7) * fz::PXS; }
 __device__ __forceinline__ int bpair(int p) { return fz::OBS + (p & 1) * 4 * fz::W; }
 __device__ __forceinline__ int brow(int j, int c) { return bpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W; }
 __device__ __forceinline__ int bprow(int r) { return fz::OBP + (r & 1) * fz::PWID; }
 __device__ __forceinline__ int rrow(int j, int c) { return fz::ORS + pmod(j, fz::RR) * 2 * fz::W + c * fz::W; }
-__device__ __forceinline__ int rprow(int r) { return fz::ORP + (r & 1) * fz::PWID; }
-__device__ __forceinline__ int arow(int j, int c) { return fz::OAS + pmod(j, fz::AR) * 2 * fz::W + c * fz::W; }
+__device__ __forceinline__ int rprow(int r) { return fz::ORP + (r & 3) * fz::PWID; }
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
@@ -590,7 +591,6 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + fz::OMB);
   unsigned phase[2] = {0u, 0u};
 
-  for (int q = t; q < fz::AR * 2 * fz::W; q += fz::kNT) sm[fz::OAS + q] = 0.0;
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -622,14 +622,34 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     tma_load_3d(sm + bpair(sB), &M.bv, xc0 + 2, 2 * sB + 1, 0, &bars[1]);
     tma_load_2d(sm + bprow(sB + 1), &M.bp, kx0 - 2, sB + 1, &bars[1]);
   }
-  mbar_wait(&bars[1], phase[1]);
-  phase[1] ^= 1u;
 
-  const int kxp = kx0 - 1 + t;  // this thread's patch column
-  double* eb = sm + fz::OEB;
+  // lane l of warp w solves strip patch pi = 30w + l (node column kxp) and, for
+  // lanes 1..30, owns lattice columns 2kxp, 2kxp+1 (ring columns 2pi+2, 2pi+3)
+  const int pi = fz::kOWN * warp + lane;
+  const int kxp = kx0 - 1 + pi;
+  const bool owner = lane >= 1 && lane <= fz::kOWN;
+  // Owner-computes accumulation in registers: carry[r][comp][col] holds the
+  // partial sums of this lane's two lattice columns on rows 2s-2+r (r = 0,1,2)
+  // entering step s; neighbour patch columns contribute through warp shuffles.
+  // Summation order is fixed (deterministic).
+  double carry[3][2][2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) carry[r][c][0] = carry[r][c][1] = 0.0;
   for (int s = sB; s <= sE; ++s) {
-    // prefetch the data of step s+1: x pair s+2 (rows 2s+5, 2s+6), p row s+3,
-    // b pair s+1 (rows 2s+3, 2s+4), b_p row s+2
+    // Data of step s (x pairs up to s+1, p rows up to s+2, b pair s, b_p row s+1)
+    // arrived on barrier (s-sB+1)&1; prefetch step s+1 into the other one.
+    // WAR safety with one CTA barrier per step (every thread has passed the
+    // barrier of step s-1, so has finished step s-1's residual; it may still
+    // be in step s-1's solve/output):
+    //   x pair s+2 -> slot of pair s-4 (read last at step s-2's output)
+    //   p row  s+3 -> slot of row  s-5;  b pair s+1 -> slot of pair s-1 (step s-1 residual)
+    //   b_p row s+2 -> slot of row s (step s-1 residual)
+    //   residual rows 2s+1, 2s+2 -> slots of rows 2s-6, 2s-5 (step s-2's solve)
+    //   pressure residual row s+1 -> slot of row s-3 (step s-3's solve)
+    mbar_wait(&bars[(s - sB + 1) & 1], phase[(s - sB + 1) & 1]);
+    phase[(s - sB + 1) & 1] ^= 1u;
     uint64_t* nbar = &bars[(s - sB) & 1];
     if (t == 0) {
       unsigned bytes = fz::kBBytes + fz::kBPBytes + (XZERO ? 0u : fz::kXBytes + fz::kPBytes);
@@ -647,20 +667,20 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     // ---- patch solve (alg:vk line 2: A_i delta_i = V_i r, exactly) ----
     double vx[25], vy[25];
     double dp = 0.0;
-    const bool valid = t < fz::kNPATCH && kxp >= 0 && kxp <= N && s >= 0 && s <= N;
+    const bool valid = kxp >= 0 && kxp <= N && s >= 0 && s <= N;
     const bool generic = kxp >= 2 && kxp <= N - 2 && s >= 2 && s <= N - 2;
     if (valid && generic) {
 #pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {  // window columns 2kxp-2.. = ring columns 2t .. 2t+4
-        const double* ru = sm + rrow(2 * s - 2 + oy, 0) + 2 * t;
-        const double* rv = sm + rrow(2 * s - 2 + oy, 1) + 2 * t;
+      for (int oy = 0; oy < 5; ++oy) {  // window columns 2kxp-2.. = ring columns 2pi .. 2pi+4
+        const double* ru = sm + rrow(2 * s - 2 + oy, 0) + 2 * pi;
+        const double* rv = sm + rrow(2 * s - 2 + oy, 1) + 2 * pi;
         const double2 u01 = lds2(ru), u23 = lds2(ru + 2), v01 = lds2(rv), v23 = lds2(rv + 2);
         vx[oy * 5 + 0] = u01.x; vx[oy * 5 + 1] = u01.y; vx[oy * 5 + 2] = u23.x; vx[oy * 5 + 3] = u23.y;
         vx[oy * 5 + 4] = ru[4];
         vy[oy * 5 + 0] = v01.x; vy[oy * 5 + 1] = v01.y; vy[oy * 5 + 2] = v23.x; vy[oy * 5 + 3] = v23.y;
         vy[oy * 5 + 4] = rv[4];
       }
-      dp = solve_generic(vx, vy, sm[rprow(s) + t + 1], F);
+      dp = solve_generic(vx, vy, sm[rprow(s) + pi + 1], F);
     } else if (valid) {  // precomputed by k_boundary_patches
       const int64_t nb = bd_count(N), bi = bd_index(kxp, s, N);
 #pragma unroll
@@ -677,127 +697,53 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
       }
     }
     // pressure: only patch k holds p_k (multiplicity 1) -> output now
-    if (t >= 1 && t <= fz::kNOUT && s >= y0 && s < y1 && kxp < g.pp) {
-      const double xp = XZERO ? 0.0 : sm[prow(s) + t + 3];
+    if (owner && s >= y0 && s < y1 && kxp < g.pp) {
+      const double xp = XZERO ? 0.0 : sm[prow(s) + pi + 3];
       A.xout[g.op + (int64_t)s * g.pp + kxp] = kxp <= N ? fma(A.omega, dp, xp) : 0.0;
     }
-    // ---- accumulate sum_i V_i^T delta_i --------------------------------
-    // patch t's window column ox is ring column 2t+ox.  Warp-local phases
-    // (own columns 2t+2,2t+3; left neighbour's 2t,2t+1; right neighbour's
-    // 2t+4); the two writes that cross a warp boundary go to the edge buffer
-    // and are folded in by their owner after the barrier (deterministic).
-    {
-      double2 a[2][5];
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) a[c][oy] = lds2(sm + arow(2 * s - 2 + oy, c) + 2 * t + 2);
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        sts2(sm + arow(2 * s - 2 + oy, 0) + 2 * t + 2, a[0][oy].x + vx[oy * 5 + 2], a[0][oy].y + vx[oy * 5 + 3]);
-        sts2(sm + arow(2 * s - 2 + oy, 1) + 2 * t + 2, a[1][oy].x + vy[oy * 5 + 2], a[1][oy].y + vy[oy * 5 + 3]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        double* e = eb + ((warp * 2 + 0) * 5 + oy) * 4;
-        e[0] = vx[oy * 5 + 0];
-        e[1] = vx[oy * 5 + 1];
-        e[2] = vy[oy * 5 + 0];
-        e[3] = vy[oy * 5 + 1];
-      }
-    } else {
-      double2 a[2][5];
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) a[c][oy] = lds2(sm + arow(2 * s - 2 + oy, c) + 2 * t);
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        sts2(sm + arow(2 * s - 2 + oy, 0) + 2 * t, a[0][oy].x + vx[oy * 5 + 0], a[0][oy].y + vx[oy * 5 + 1]);
-        sts2(sm + arow(2 * s - 2 + oy, 1) + 2 * t, a[1][oy].x + vy[oy * 5 + 0], a[1][oy].y + vy[oy * 5 + 1]);
-      }
-    }
-    __syncwarp();
-    if (lane == 31) {
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        double* e = eb + ((warp * 2 + 1) * 5 + oy) * 4;
-        e[0] = vx[oy * 5 + 4];
-        e[2] = vy[oy * 5 + 4];
-      }
-    } else {
-      double a[2][5];
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) a[c][oy] = sm[arow(2 * s - 2 + oy, c) + 2 * t + 4];
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        sm[arow(2 * s - 2 + oy, 0) + 2 * t + 4] = a[0][oy] + vx[oy * 5 + 4];
-        sm[arow(2 * s - 2 + oy, 1) + 2 * t + 4] = a[1][oy] + vy[oy * 5 + 4];
-      }
-    }
-    __syncthreads();
-    if (lane == 31 && warp + 1 < fz::kWarps) {  // left part sent by the next warp's lane 0
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        const double* e = eb + (((warp + 1) * 2 + 0) * 5 + oy) * 4;
-        double* au = sm + arow(2 * s - 2 + oy, 0) + 2 * t + 2;
-        double* av = sm + arow(2 * s - 2 + oy, 1) + 2 * t + 2;
-        au[0] += e[0];
-        au[1] += e[1];
-        av[0] += e[2];
-        av[1] += e[3];
-      }
-    }
-    if (lane == 0 && warp > 0) {  // right part sent by the previous warp's lane 31
-#pragma unroll
-      for (int oy = 0; oy < 5; ++oy) {
-        const double* e = eb + (((warp - 1) * 2 + 1) * 5 + oy) * 4;
-        sm[arow(2 * s - 2 + oy, 0) + 2 * t + 2] += e[0];
-        sm[arow(2 * s - 2 + oy, 1) + 2 * t + 2] += e[2];
-      }
-    }
-
-    // ---- lattice rows 2s-2, 2s-1 (node row s-1) are complete ----
-    // thread t owns node column kxp: lattice columns 2kxp, 2kxp+1 = ring columns 2t+2, 2t+3
+    // ---- sum_i V_i^T delta_i on this lane's columns, lattice rows 2s-2 .. 2s+2,
+    //      and x_out on rows 2s-2, 2s-1 (node row s-1), which are now complete ----
     const int ny = s - 1;
-    if (t >= 1 && t <= fz::kNOUT && ny >= y0 && ny < y1 && 2 * kxp < g.pu) {
+    const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
+    const int i0 = 2 * kxp;
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int j = 2 * ny + rr;
-        if (j > lat - 1) continue;
-        const int i0 = 2 * kxp;
-        const bool jin = j >= 1 && j <= lat - 2;
-        // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
-        const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
-        const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
-        const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
-        const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
+    for (int c = 0; c < 2; ++c) {
+      const double* v = c ? vy : vx;
+      double S0[5], S1[5];
 #pragma unroll
-        for (int comp = 0; comp < 2; ++comp) {
-          const double2 a = lds2(sm + arow(j, comp) + 2 * t + 2);
-          const double2 x = XZERO ? make_double2(0.0, 0.0) : lds2(sm + xrow(j, comp) + 2 * t + 4);
-          const double o0 = in0 ? fma(w0, a.x, x.x) : (i0 <= lat - 1 ? x.x : 0.0);
-          const double o1 = in1 ? fma(w1, a.y, x.y) : (i0 + 1 <= lat - 1 ? x.y : 0.0);
-          *reinterpret_cast<double2*>(A.xout + (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
-              make_double2(o0, o1);
+      for (int oy = 0; oy < 5; ++oy) {
+        const double r0 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 0], 1);  // patch pi+1, window column 0
+        const double r1 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 1], 1);  // patch pi+1, window column 1
+        const double l4 = __shfl_up_sync(0xffffffffu, v[oy * 5 + 4], 1);    // patch pi-1, window column 4
+        S0[oy] = (oy < 3 ? carry[oy][c][0] : 0.0) + v[oy * 5 + 2] + l4 + r0;
+        S1[oy] = (oy < 3 ? carry[oy][c][1] : 0.0) + v[oy * 5 + 3] + r1;
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        carry[r][c][0] = S0[r + 2];
+        carry[r][c][1] = S1[r + 2];
+      }
+      if (rowout) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int j = 2 * ny + rr;
+          if (j > lat - 1) continue;
+          const bool jin = j >= 1 && j <= lat - 2;
+          // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
+          const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
+          const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
+          const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
+          const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
+          const double2 x = XZERO ? make_double2(0.0, 0.0) : lds2(sm + xrow(j, c) + 2 * pi + 4);
+          const double o0 = in0 ? fma(w0, S0[rr], x.x) : (i0 <= lat - 1 ? x.x : 0.0);
+          const double o1 = in1 ? fma(w1, S1[rr], x.y) : (i0 + 1 <= lat - 1 ? x.y : 0.0);
+          *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) = make_double2(o0, o1);
         }
       }
     }
-    mbar_wait(nbar, phase[(s - sB) & 1]);
-    phase[(s - sB) & 1] ^= 1u;
-    __syncthreads();
-    // clear the two finished accumulator rows for reuse
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      sts2(sm + arow(2 * ny, c) + 2 * t, 0.0, 0.0);
-      sts2(sm + arow(2 * ny + 1, c) + 2 * t, 0.0, 0.0);
-    }
   }
+  // the last prefetch (for step sE+1) must land before the CTA's shared memory is released
+  mbar_wait(&bars[(sE - sB) & 1], phase[(sE - sB) & 1]);
 }
 
 inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const double* /*d_inv*/, double* d_fac,
