@@ -18,6 +18,7 @@
 #include "kernels_common.cuh"
 #include "krylov.cuh"
 #include "sweep_fused.cuh"
+#include "residual_strip.cuh"
 
 using namespace svk;
 
@@ -214,10 +215,21 @@ int alloc_vec(svk_ctx* ctx, double** p, int64_t n) {
 }
 
 // ------------------------------------------------------------------ level ops
+// r = b - A x (b != NULL) or r = A x (b == NULL), streaming strip kernel
 int op_residual(svk_ctx* ctx, int l, const double* x, const double* b, double* r, cudaStream_t s) {
-  const LevelGeom& g = ctx->g[l];
-  if (b) k_residual<true><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.nu, x, b, r);
-  else k_residual<false><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.nu, x, nullptr, r);
+  if (launch_residual_strip(ctx->g[l], nullptr, ctx->h_fac[l], x, b, r, ctx->nsm, s) != 0) {
+    ctx->err = "residual: TMA descriptor encoding failed";
+    return SVK_ERR_CUDA;
+  }
+  CKL();
+  return SVK_OK;
+}
+// r_c = P^T (b - A x) on level l-1 in one pass (alg:mg lines 3-4)
+int op_residual_restrict(svk_ctx* ctx, int l, const double* x, const double* b, double* rc, cudaStream_t s) {
+  if (launch_residual_strip(ctx->g[l], &ctx->g[l - 1], ctx->h_fac[l], x, b, rc, ctx->nsm, s) != 0) {
+    ctx->err = "residual+restrict: TMA descriptor encoding failed";
+    return SVK_ERR_CUDA;
+  }
   CKL();
   return SVK_OK;
 }
@@ -305,8 +317,7 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
     std::swap(cur, oth);
   }
   if (ctx->cfg.nu_pre == 0 && x_zero) CK(cudaMemsetAsync(cur, 0, g.len * sizeof(double), s));
-  TRY(op_residual(ctx, l, cur, b, ctx->ws_r[l], s));          // "Compute residual"
-  TRY(op_restrict(ctx, l, ctx->ws_r[l], ctx->ws_b[l - 1], s)); // "Restriction"
+  TRY(op_residual_restrict(ctx, l, cur, b, ctx->ws_b[l - 1], s));  // "Compute residual" + "Restriction"
   TRY(op_mg(ctx, l - 1, ctx->ws_b[l - 1], ctx->ws_x[l - 1], true, s));  // A_0^{-1} or MG(l-1)
   TRY(op_prolong_add(ctx, l, ctx->ws_x[l - 1], cur, s));       // "Correction"
   for (int k = 0; k < ctx->cfg.nu_post; ++k) {                 // "Relax on u_l and p_l"

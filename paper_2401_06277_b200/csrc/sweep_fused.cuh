@@ -354,10 +354,9 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) { *reinterpr
 // node (kx0-2+t, sp+1).  Reads x rows 2sp..2sp+4, p rows sp..sp+2, b rows
 // 2sp+1, 2sp+2 (pair sp), b_p row sp+1.  Each stencil coefficient is loaded once
 // and used for both components; the whole 5x5 windows are loaded first.
-template <bool XZERO>
-__device__ __forceinline__ void fused_residual(double* sm, const FusedArgs& A, const FusedFactors& F, int sp,
+template <bool XZERO, bool NOB = false, int RRN = fz::RR, int ORSB = fz::ORS, int ORPB = fz::ORP>
+__device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
                                                int kx0) {
-  const LevelGeom& g = A.g;
   const int N = g.N, lat = g.lat, t = threadIdx.x;
   const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
@@ -454,16 +453,18 @@ __device__ __forceinline__ void fused_residual(double* sm, const FusedArgs& A, c
     ax[7] += F.GY[0][1][0][0] * Pm[0][1] + F.GY[0][1][0][1] * Pm[0][2] + F.GY[0][1][2][0] * Pm[2][1] +
              F.GY[0][1][2][1] * Pm[2][2];
   }
-  // r = b - A x on non-Dirichlet points (b columns rc0.. = 2t, 2t+1 of the b ring)
+  // r = b - A x on non-Dirichlet points (b columns rc0.. = 2t, 2t+1 of the b ring); NOB: b = 0
+  auto rr = [&](int j, int c) { return ORSB + pmod(j, RRN) * 2 * fz::W + c * fz::W; };
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    const double2 b0 = lds2(sm + brow(j0, comp) + 2 * t), b1 = lds2(sm + brow(j1, comp) + 2 * t);
-    sts2(sm + rrow(j0, comp) + 2 * t, (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0,
+    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j0, comp) + 2 * t);
+    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j1, comp) + 2 * t);
+    sts2(sm + rr(j0, comp) + 2 * t, (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0,
          (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0);
-    sts2(sm + rrow(j1, comp) + 2 * t, (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0,
+    sts2(sm + rr(j1, comp) + 2 * t, (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0,
          (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0);
   }
-  sm[rprow(nrow) + t] = pok ? sm[bprow(nrow) + t] - bu : 0.0;
+  sm[ORPB + (nrow & 3) * fz::PWID + t] = pok ? (NOB ? 0.0 : sm[bprow(nrow) + t]) - bu : 0.0;
 }
 
 // forward even/odd transform of one 5-vector with stride st (in place)
@@ -611,8 +612,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   }
   mbar_wait(&bars[0], phase[0]);
   phase[0] ^= 1u;
-  fused_residual<XZERO>(sm, A, F, sB - 2, kx0);
-  fused_residual<XZERO>(sm, A, F, sB - 1, kx0);
+  fused_residual<XZERO>(sm, A.g, F, sB - 2, kx0);
+  fused_residual<XZERO>(sm, A.g, F, sB - 1, kx0);
   __syncthreads();
   // data of step sB: p row sB+2, b pair sB, b_p row sB+1 -> barrier 1
   if (t == 0) {
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
       tma_load_3d(sm + bpair(s + 1), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
       tma_load_2d(sm + bprow(s + 2), &M.bp, kx0 - 2, s + 2, nbar);
     }
-    fused_residual<XZERO>(sm, A, F, s, kx0);
+    fused_residual<XZERO>(sm, A.g, F, s, kx0);
     __syncthreads();
 
     // ---- patch solve (alg:vk line 2: A_i delta_i = V_i r, exactly) ----
