@@ -98,3 +98,101 @@ __global__ void k_scale(double* __restrict__ dst, const double* __restrict__ src
 }
 
 }  // namespace svk
+
+namespace svk {
+
+// ---------------------------------------------------------------------------
+// Fused classical Gram-Schmidt passes (CGS2) over a device array of basis
+// pointers V[0..m), m <= kCgsMax.  Every pass reads each basis vector once:
+//   k_cgs_dots  : part[i] = V_i . w                                   (i < m)
+//   k_cgs_update: w_out = w - sum_i c_i V_i; DOTS: part[i] = V_i . w_out (i < m);
+//                 always part[m] (DOTS) or part[0] = w_out . w_out
+// Per-block partials (fixed grid) are reduced by k_reduce_partials in a fixed
+// order, so results are deterministic.  One element per thread per iteration
+// keeps the m basis values in registers between the update and the dots.
+// ---------------------------------------------------------------------------
+constexpr int kCgsMax = 32;
+struct VecList {  // basis pointers by value (kernel-parameter space)
+  const double* p[kCgsMax];
+};
+
+template <int MM>
+__device__ __forceinline__ void block_reduce_store_n(const double (&acc)[MM], int m_used, double extra, int extra_at,
+                                                     double* __restrict__ partial, int stride) {
+  __shared__ double smr[kRedThreads / 32][MM + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m <= MM; ++m) {
+    const bool use = m < MM ? (m < m_used) : (extra_at >= 0);
+    if (!use) continue;
+    double v = m < MM ? acc[m] : extra;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) smr[wid][m] = v;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < m_used; m += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += smr[w][m];
+    partial[m * stride + blockIdx.x] = s;
+  }
+  if (extra_at >= 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += smr[w][MM];
+    partial[extra_at * stride + blockIdx.x] = s;
+  }
+}
+
+// part[i] = V_i . w for i < m <= MM (double2 streaming, high occupancy)
+template <int MM>
+__global__ void __launch_bounds__(kRedThreads) k_cgs_dots(const VecList V, int m, const double* __restrict__ w,
+                                                          int64_t n, double* __restrict__ partial) {
+  double acc[MM];
+#pragma unroll
+  for (int i = 0; i < MM; ++i) acc[i] = 0.0;
+  const int64_t n2 = n >> 1;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 wq = w2[q];
+#pragma unroll
+    for (int i = 0; i < MM; ++i)
+      if (i < m) {
+        const double2 v = reinterpret_cast<const double2*>(V.p[i])[q];
+        acc[i] = fma(v.x, wq.x, fma(v.y, wq.y, acc[i]));
+      }
+  }
+  block_reduce_store_n<MM>(acc, m, 0.0, -1, partial, gridDim.x);
+}
+
+// w_out = w - sum_{i<m} c_i V_i (m <= kCgsMax); part[0] = w_out . w_out
+__global__ void __launch_bounds__(kRedThreads) k_cgs_update(const VecList V, int m, const double* __restrict__ c,
+                                                            const double* __restrict__ w, double* __restrict__ wout,
+                                                            int64_t n, double* __restrict__ partial) {
+  const int64_t n2 = n >> 1;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(wout);
+  double nrm = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = w2[q];
+#pragma unroll 8
+    for (int i = 0; i < m; ++i) {
+      const double ci = __ldg(c + i);
+      const double2 v = reinterpret_cast<const double2*>(V.p[i])[q];
+      a.x = fma(-ci, v.x, a.x);
+      a.y = fma(-ci, v.y, a.y);
+    }
+    o2[q] = a;
+    nrm = fma(a.x, a.x, fma(a.y, a.y, nrm));
+  }
+  double dummy[1] = {0.0};
+  block_reduce_store_n<1>(dummy, 0, nrm, 0, partial, gridDim.x);
+}
+
+// c[i] = raw[i] * scale[i]  (device), for i < m
+__global__ void k_scale_coef(const double* __restrict__ raw, const double* __restrict__ scale, double* __restrict__ c,
+                             int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) c[i] = raw[i] * scale[i];
+}
+
+}  // namespace svk

@@ -45,6 +45,7 @@ struct svk_ctx {
   double* d_w = nullptr;
   double* d_r = nullptr;
   double* d_part = nullptr;
+  double* d_part2 = nullptr;
   double* d_coef = nullptr;
   double* h_pin = nullptr;
   int coef_cap = 0;
@@ -372,6 +373,53 @@ int host_norm(svk_ctx* ctx, const double* v, int64_t n, double* out, cudaStream_
   return SVK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Gram-Schmidt passes; basis pointers are passed by value (kernel-parameter space).
+// out[0..m) = V_i . w (deterministic), written to d_coef + off.
+VecList veclist(const double* const* v, int m) {
+  VecList L{};
+  for (int i = 0; i < m && i < kCgsMax; ++i) L.p[i] = v[i];
+  return L;
+}
+int cgs_dots(svk_ctx* ctx, const double* const* dV, int m, const double* w, int64_t n, int off, cudaStream_t s) {
+  constexpr int kDot = 16;
+  for (int c0 = 0; c0 < m; c0 += kDot) {
+    const int mm = std::min(kDot, m - c0);
+    if (mm <= 4) k_cgs_dots<4><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
+    else if (mm <= 8) k_cgs_dots<8><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
+    else k_cgs_dots<16><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
+    CKL();
+    k_reduce_partials<<<mm, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + off + c0, 0);
+    CKL();
+  }
+  return SVK_OK;
+}
+// w_out = w - sum_i c_i V_i (c at d_coef + coff); squared norm of w_out -> d_coef + noff (if noff >= 0)
+int cgs_update(svk_ctx* ctx, const double* const* dV, int m, int coff, const double* w, double* wout, int64_t n,
+               int noff, cudaStream_t s) {
+  const double* src = w;
+  if (m == 0 && w != wout) CK(cudaMemcpyAsync(wout, w, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (int c0 = 0; c0 < m; c0 += kCgsMax) {
+    const int mm = std::min(kCgsMax, m - c0);
+    k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, ctx->d_coef + coff + c0, src, wout, n,
+                                                     ctx->d_part);
+    CKL();
+    src = wout;
+  }
+  if (noff >= 0) {
+    k_reduce_partials<<<1, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + noff, 0);
+    CKL();
+  }
+  return SVK_OK;
+}
+
+// Right-preconditioned flexible GMRES with an un-normalised
+// Arnoldi basis: V~_j = n_j v_j and Z~_j = M V~_j = n_j z_j are stored without
+// scaling (the V-cycle from zero is linear), so no vector pass is spent on
+// normalisation; the scales n_j live on the host and enter the Hessenberg:
+//   w~ = A Z~_j = n_j A z_j;  CGS2: w~'' = w~ - sum_i C_i V~_i  (C = c1 + c2,
+//   c_k,i = (V~_i . w) / n_i^2);  h_ij = C_i n_i / n_j;  h_j+1,j = |w~''| / n_j;
+//   V~_j+1 = w~'', n_j+1 = |w~''|;  x = x0 + sum_i (y_i / n_i) Z~_i.
 int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit, double* hist, svk_report* rep,
                 cudaStream_t s) {
   auto t0 = std::chrono::steady_clock::now();
@@ -380,12 +428,26 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   const int64_t n = g.len;
   svk_report R{};
   double tv = 0, to = 0;
-  TRY(ensure_coef(ctx, 3 * (maxit + 2) + 8));
-  if (!ctx->d_r) TRY(alloc_vec(ctx, &ctx->d_r, n));
+  // coefficient area: [c1 (maxit+1) | c2 (maxit+1) | raw (maxit+1) | nrm | n^-2 (maxit+1)]
+  const int o1 = 0, o2 = maxit + 1, oraw = 2 * (maxit + 1), onrm = 3 * (maxit + 1), oinv = 3 * (maxit + 1) + 1;
+  TRY(ensure_coef(ctx, 4 * (maxit + 1) + 8));
   if (!ctx->d_w) TRY(alloc_vec(ctx, &ctx->d_w, n));
-  TRY(op_residual(ctx, L, x, b, ctx->d_r, s));
-  double beta;
-  TRY(host_norm(ctx, ctx->d_r, n, &beta, s));
+  if (!ctx->d_r) TRY(alloc_vec(ctx, &ctx->d_r, n));
+  auto ensure_vec = [&](std::vector<double*>& pool, int k) -> int {
+    while ((int)pool.size() <= k) {
+      double* p;
+      TRY(alloc_vec(ctx, &p, n));
+      pool.push_back(p);
+    }
+    return SVK_OK;
+  };
+  TRY(ensure_vec(ctx->V, 0));
+  // V~_0 = r0 = b - A x0, n_0 = |r0|
+  TRY(op_residual(ctx, L, x, b, ctx->V[0], s));
+  TRY(cgs_dots(ctx, (const double* const*)ctx->V.data(), 1, ctx->V[0], n, onrm, s));
+  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef + onrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double beta = std::sqrt(std::max(ctx->h_pin[0], 0.0));
   if (hist) hist[0] = 1.0;
   if (!std::isfinite(beta)) {
     ctx->err = "non-finite initial residual";
@@ -393,52 +455,54 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   }
   int status = SVK_OK, k = 0;
   bool conv = beta == 0.0;
-  std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), gv(maxit + 1, 0.0);
+  std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), gv(maxit + 1, 0.0), nv(maxit + 2);
+  std::vector<double> inv_nsq(maxit + 1);
   auto Hij = [&](int i, int j) -> double& { return H[(size_t)i * maxit + j]; };
   if (!conv) {
     gv[0] = beta;
-    if (ctx->V.empty()) {
-      double* p;
-      TRY(alloc_vec(ctx, &p, n));
-      ctx->V.push_back(p);
-    }
-    k_scale<<<kDotBlocks, 256, 0, s>>>(ctx->V[0], ctx->d_r, 1.0 / beta, n);
-    CKL();
-    const int o1 = 0, o2 = maxit + 1, on = 2 * (maxit + 1);
+    nv[0] = beta;
+    inv_nsq[0] = 1.0 / (beta * beta);
     for (int j = 0; j < maxit; ++j) {
-      if ((int)ctx->Z.size() <= j) {
-        double* p;
-        TRY(alloc_vec(ctx, &p, n));
-        ctx->Z.push_back(p);
-      }
-      // z_j = M v_j : one V-cycle from zero
+      const int m = j + 1;
+      TRY(ensure_vec(ctx->Z, j));
+      TRY(ensure_vec(ctx->V, j + 1));
+      // basis pointers and scales for this iteration (small H2D copies, stream ordered)
+      std::memcpy(ctx->h_pin, inv_nsq.data(), m * sizeof(double));
+      CK(cudaMemcpyAsync(ctx->d_coef + oinv, ctx->h_pin, m * sizeof(double), cudaMemcpyHostToDevice, s));
+      const double* const* hV = (const double* const*)ctx->V.data();
+      // z~_j = M V~_j : one V-cycle from zero
       CK(cudaEventRecord(ctx->ev[0], s));
       TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
       CK(cudaEventRecord(ctx->ev[1], s));
-      // w = A z_j ; CGS2 against v_0..v_j ; ||w||
+      // w~ = A z~_j ; CGS2 against V~_0..V~_j ; |w~''|
       TRY(op_residual(ctx, L, ctx->Z[j], nullptr, ctx->d_w, s));
-      std::vector<const double*> vs(ctx->V.begin(), ctx->V.begin() + j + 1);
-      TRY(op_dots(ctx, vs, ctx->d_w, n, o1, s));
-      TRY(op_axpys(ctx, ctx->d_w, vs, o1, -1.0, n, s));
-      TRY(op_dots(ctx, vs, ctx->d_w, n, o2, s));
-      TRY(op_axpys(ctx, ctx->d_w, vs, o2, -1.0, n, s));
-      TRY(op_dots(ctx, {ctx->d_w}, ctx->d_w, n, on, s));
+      TRY(cgs_dots(ctx, hV, m, ctx->d_w, n, oraw, s));
+      k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
+      CKL();
+      TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->d_w, n, -1, s));
+      TRY(cgs_dots(ctx, hV, m, ctx->d_w, n, oraw, s));
+      k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
+      CKL();
+      TRY(cgs_update(ctx, hV, m, o2, ctx->d_w, ctx->V[j + 1], n, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
-      CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (3 * (maxit + 1)) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       float a01 = 0, a12 = 0;
       cudaEventElapsedTime(&a01, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&a12, ctx->ev[1], ctx->ev[2]);
       tv += a01 * 1e-3;
       to += a12 * 1e-3;
-      for (int i = 0; i <= j; ++i) Hij(i, j) = ctx->h_pin[o1 + i] + ctx->h_pin[o2 + i];
-      const double hn = std::sqrt(std::max(ctx->h_pin[on], 0.0));
+      for (int i = 0; i <= j; ++i) Hij(i, j) = (ctx->h_pin[o1 + i] + ctx->h_pin[o2 + i]) * nv[i] / nv[j];
+      const double nn = std::sqrt(std::max(ctx->h_pin[onrm], 0.0));
+      const double hn = nn / nv[j];
       if (!std::isfinite(hn)) {
         status = SVK_ERR_NONFINITE;
         ctx->err = "non-finite Arnoldi vector";
         k = j;
         break;
       }
+      nv[j + 1] = nn;
+      if (j + 1 <= maxit) inv_nsq[j + 1] = nn > 0 ? 1.0 / (nn * nn) : 0.0;
       Hij(j + 1, j) = hn;
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
@@ -459,25 +523,22 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
         conv = true;
         break;
       }
-      if ((int)ctx->V.size() <= j + 1) {
-        double* p;
-        TRY(alloc_vec(ctx, &p, n));
-        ctx->V.push_back(p);
-      }
-      k_scale<<<kDotBlocks, 256, 0, s>>>(ctx->V[j + 1], ctx->d_w, 1.0 / hn, n);
-      CKL();
     }
-    if (k > 0) {
+    if (k > 0) {  // x += sum_i (y_i / n_i) Z~_i  (as w_out = w - sum c_i V_i with c_i = -y_i / n_i)
       std::vector<double> y(k);
       for (int i = k - 1; i >= 0; --i) {
         double t = gv[i];
-        for (int m = i + 1; m < k; ++m) t -= Hij(i, m) * y[m];
+        for (int mm = i + 1; mm < k; ++mm) t -= Hij(i, mm) * y[mm];
         y[i] = t / Hij(i, i);
       }
-      std::memcpy(ctx->h_pin, y.data(), k * sizeof(double));
-      CK(cudaMemcpyAsync(ctx->d_coef, ctx->h_pin, k * sizeof(double), cudaMemcpyHostToDevice, s));
-      std::vector<const double*> zs(ctx->Z.begin(), ctx->Z.begin() + k);
-      TRY(op_axpys(ctx, x, zs, 0, 1.0, n, s));
+      for (int i = 0; i < k; ++i) ctx->h_pin[i] = -y[i] / nv[i];
+      CK(cudaMemcpyAsync(ctx->d_coef + o1, ctx->h_pin, k * sizeof(double), cudaMemcpyHostToDevice, s));
+      for (int c0 = 0; c0 < k; c0 += kCgsMax) {
+        const int mm = std::min(kCgsMax, k - c0);
+        k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist((const double* const*)ctx->Z.data() + c0, mm), mm,
+                                                         ctx->d_coef + o1 + c0, x, x, n, ctx->d_part);
+        CKL();
+      }
     }
   }
   double rn = 0.0;
@@ -517,6 +578,7 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_w);
   F(ctx->d_r);
   F(ctx->d_part);
+  F(ctx->d_part2);
   F(ctx->d_coef);
   F(ctx->d_hb);
   F(ctx->d_hx);
@@ -614,7 +676,8 @@ int create_impl(svk_ctx* ctx) {
     const LevelGeom& gf = ctx->g.back();
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
   }
-  CK(cudaMalloc(&ctx->d_part, (size_t)kMaxM * kDotBlocks * sizeof(double)));
+  CK(cudaMalloc(&ctx->d_part, (size_t)(kCgsMax + 1) * kDotBlocks * sizeof(double)));
+  CK(cudaMalloc(&ctx->d_part2, (size_t)(kCgsMax + 1) * sizeof(double)));
   CK(cudaDeviceSynchronize());
   return SVK_OK;
 }
