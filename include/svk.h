@@ -208,9 +208,9 @@ int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y,
  * benchmark's gpu_launches count). */
 int64_t svk_launch_count(const svk_ctx* ctx);
 
-/* Benchmark support.  While profiling is enabled, every Vanka sweep on the
- * finest level (the kernels of one svk_vanka_sweep step: the boundary-patch
- * kernel and the fused sweep, or the three unfused kernels) is bracketed by
+/* Benchmark support.  While profiling is enabled, every full Vanka sweep (non-
+ * zero initial guess) on the finest level (the kernels of one sweep step: the
+ * boundary-patch kernel and the fused sweep, or the three unfused kernels) is bracketed by
  * CUDA events recorded on the sweep's stream.  svk_sweep_stats synchronises
  * the device, returns the number of bracketed sweeps and their summed device
  * time in milliseconds since the previous call, and resets both. */

@@ -238,7 +238,8 @@ int op_residual_restrict(svk_ctx* ctx, int l, const double* x, const double* b, 
 int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero,
                   cudaStream_t s);
 int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
-  const bool timed = ctx->prof && l == ctx->nlev - 1;
+  // only full sweeps (non-zero x_in) are timed, so the roofline's per-unit counts apply
+  const bool timed = ctx->prof && l == ctx->nlev - 1 && !x_zero;
   if (timed) {
     while (ctx->prof_ev.size() < ctx->prof_used + 2) {
       cudaEvent_t e;
