@@ -12,16 +12,18 @@ level-0 solve, V-cycle, FGMRES.  The hierarchy + patch setup (svk_create) runs o
 per context, as the paper precomputes its patch inverses; its time is
 reported as `setup_s`.
 
-value  = DOFs solved per second (whole job: N GPUs x one 4096^2 problem each).
+value  = DOFs solved per second (whole job).
 sweep  = the finest-level Vanka sweeps inside the timed solves (CUDA events on the
          sweep stream, svk_set_profiling): DOF/s, algorithmic HBM GB/s, roofline.
 e2e    = the same solve through svk_solve_host with pinned HOST buffers (H2D of
          b and x0, D2H of x inside the timed region).
 --impl reference  times the CPU oracle (oracle/, C++ + OpenMP, fp64) on a bounded
          sample of the same workload (a 256^2 solve per step) on the host cores.
-Multi-GPU (N > 1, torchrun): until the row-slab layer lands every rank solves its
-own 4096^2 problem (independent replicas, weak scaling, no data-path collective);
-time = max over ranks.
+Multi-GPU (N > 1, torchrun): `--mode slabs` (default) splits the ONE 4096^2
+problem into N row slabs (libsvk multi-GPU mode over NCCL: halo exchanges,
+coarse-level agglomeration, all-reduced Krylov dots; strong scaling);
+`--mode replicas` solves an independent 4096^2 problem per rank (weak scaling).
+Time = max over ranks.
 """
 from __future__ import annotations
 
@@ -151,8 +153,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args),
+        "higher_is_better": True, "scaling": "strong" if world > 1 and args.mode == "slabs" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, world),
         "iterations": its,
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "oracle",
                          "sample": "FGMRES+V(1,1)-Vanka solve of the %d^2 MMS problem per step (oracle C++/OpenMP, "
@@ -163,12 +166,14 @@ def run_reference(args):
     return 0
 
 
-def config_dict(args):
+def config_dict(args, world=1):
     return {"workload": "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka"
                         % (args.n, args.n),
             "N": args.n, "levels_to": 4, "dofs": n_dof(args.n), "omega_v": 0.8, "weighting": "multiplicity",
             "sweep_impl": args.sweep, "l2": "inputs exceed L2 (%.2f GB per vector vs 126 MB L2)"
-            % (n_dof(args.n) * 8 / 1e9), "parallelism": "replicas%d" % args.gpus}
+            % (n_dof(args.n) * 8 / 1e9),
+            "parallelism": ("slabs%d" % world) if world > 1 and args.mode == "slabs" else "replicas%d" % world,
+            "agglom_rows": args.agglom}
 
 
 def cpu_baseline(args):
@@ -198,8 +203,15 @@ def run_svk(args):
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
     N = args.n
+    slabs = world > 1 and args.mode == "slabs"
     t0 = time.perf_counter()
-    S = Solver(N, sweep=args.sweep, device=dev)
+    if slabs:
+        from paper_2401_06277_b200 import svk
+        nid = svk.nccl_id_broadcast()
+        S = Solver(N, sweep=args.sweep, device=dev, rank=rank, nranks=world, transport="nccl",
+                   agglom_rows=args.agglom, nccl_id=nid)
+    else:
+        S = Solver(N, sweep=args.sweep, device=dev)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     b, x0 = S.set_problem("mms_paper")
@@ -239,13 +251,16 @@ def run_svk(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     ms_step = 1e3 * t / args.steps
-    value = world * n_dof(N) * args.steps / t
+    jobs = 1 if slabs else world  # problems solved per step by the whole job
+    value = jobs * n_dof(N) * args.steps / t
     its = [r["iterations"] for r in reps]
 
     # sweep roofline (dominant kernel)
     t_sweep = sw_ms / 1e3 / max(nsw, 1)
-    nodes = (N + 1) ** 2
-    bytes_alg = 3 * 8 * n_dof(N)
+    r0, r1, _ = S.owned_rows()
+    share = (r1 - r0) / (N + 1)  # this rank's slab of the sweep (1 on a single GPU)
+    nodes = (N + 1) ** 2 * share
+    bytes_alg = 3 * 8 * n_dof(N) * share
     hbm_peak, hbm_src = measured_peaks()
     sweep_gbs = bytes_alg / t_sweep / 1e9
     flops = FLOPS_PER_NODE * nodes
@@ -280,8 +295,8 @@ def run_svk(args):
             tt = torch.tensor([tmax], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tmax = float(tt.item())
-        e2e = {"value": world * n_dof(N) * args.e2e_steps / tmax, "unit": "DOF/s",
-               "h2d_bytes_per_step": 2 * n_dof(N) * 8, "d2h_bytes_per_step": n_dof(N) * 8,
+        e2e = {"value": jobs * n_dof(N) * args.e2e_steps / tmax, "unit": "DOF/s",
+               "h2d_bytes_per_step": world * 2 * n_dof(N) * 8, "d2h_bytes_per_step": world * n_dof(N) * 8,
                "steps": args.e2e_steps, "ms_per_step": 1e3 * tmax / args.e2e_steps,
                "api": "svk_solve_host (compact host arrays, pinned)"}
 
@@ -292,13 +307,14 @@ def run_svk(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if slabs else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper manufactured solution, P:76-81)",
-            "config": config_dict(args),
+            "config": config_dict(args, world),
             "time_to_solve_s": ms_step / 1e3, "iterations": its[-1], "iterations_all": its,
             "rel_residual": reps[-1]["rel_residual"], "setup_s": setup_s,
             "t_vcycle_s": reps[-1]["t_vcycle_s"], "t_orth_s": reps[-1]["t_orth_s"],
-            "sweep": {"dof_per_s": n_dof(N) / t_sweep, "ms": 1e3 * t_sweep, "hbm_gbs_alg": sweep_gbs,
+            "sweep": {"dof_per_s": n_dof(N) * share / t_sweep, "slab_share": share, "ms": 1e3 * t_sweep, "hbm_gbs_alg": sweep_gbs,
                       "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         }
@@ -323,6 +339,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=512)
     ap.add_argument("--ref-n", type=int, default=256)
+    ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs")
+    ap.add_argument("--agglom", type=int, default=64)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -44,6 +44,14 @@
  *
  * THREADING.  One context per device; calls on one context must not overlap
  * (scratch is per context).  Different contexts are independent.
+ *
+ * MULTI-GPU (nranks > 1).  Every rank creates one context with the same
+ * configuration except `rank`.  The finest levels are split into row slabs;
+ * every call then computes only the rank's owned rows, and the library refreshes
+ * halo rows (3 node rows per side) of its input vectors itself, so rows outside
+ * a rank's slab are library-managed scratch.  svk_fgmres / svk_vcycle /
+ * svk_vanka_sweep / svk_residual / svk_matvec must be called by all ranks
+ * together (they communicate).  svk_allgather assembles a full vector.
  */
 #ifndef SVK_H_
 #define SVK_H_
@@ -102,8 +110,25 @@ typedef struct svk_config {
   int32_t coarse;     /* enum svk_coarse; default EXACT */
   int32_t sweep_impl; /* enum svk_sweep_impl; default FUSED */
   int32_t device;     /* CUDA device ordinal; default 0 */
-  int32_t reserved[8];
+  /* multi-GPU row slabs (the paper is single-GPU): */
+  int32_t rank;        /* this process's rank; default 0 */
+  int32_t nranks;      /* number of ranks; default 1 (no communication) */
+  int32_t transport;   /* enum svk_transport; default NONE */
+  int32_t agglom_rows; /* levels with fewer than agglom_rows node rows per rank are
+                          replicated on every rank (coarse agglomeration); default 64, >= 4 */
+  int32_t emul_group;  /* EMULATED transport: id of the in-process group to join */
+  int32_t reserved[3];
+  uint8_t nccl_id[128]; /* NCCL transport: ncclUniqueId from svk_nccl_unique_id() on rank 0,
+                           broadcast to every rank by the caller */
 } svk_config;
+
+/* transports for nranks > 1:
+ * NCCL     -- one process per GPU; halos by ncclSend/ncclRecv with the two slab
+ *             neighbours, dot products by ncclAllReduce (libnccl.so.2 is loaded
+ *             with dlopen on first use);
+ * EMULATED -- nranks logical ranks inside ONE process on one device, one host
+ *             thread per rank (test mode; same partition, halos and reductions). */
+enum svk_transport { SVK_TRANSPORT_NONE = 0, SVK_TRANSPORT_NCCL = 1, SVK_TRANSPORT_EMULATED = 2 };
 
 typedef struct svk_level {
   int32_t N;          /* elements per side on this level */
@@ -113,6 +138,10 @@ typedef struct svk_level {
   int64_t pitch_u, pitch_p;       /* row pitches (doubles), multiples of 8 */
   int64_t n_dof;      /* 2(2N+1)^2 + (N+1)^2 (Dirichlet DOFs included) */
   int64_t n_patch;    /* (N+1)^2 Vanka patches, one per pressure node */
+  int32_t row0, row1; /* owned node rows [row0, row1) of this rank (lattice rows
+                         [2 row0, min(2 row1, lat))); 0, N+1 on a single rank */
+  int32_t distributed; /* 1 if this level is split into row slabs */
+  int32_t halo_rows;   /* node rows of halo refreshed per side (0 if not distributed) */
 } svk_level;
 
 typedef struct svk_report {
@@ -216,6 +245,21 @@ int64_t svk_launch_count(const svk_ctx* ctx);
  * time in milliseconds since the previous call, and resets both. */
 int svk_set_profiling(svk_ctx* ctx, int32_t enable);
 int svk_sweep_stats(svk_ctx* ctx, int64_t* count, double* total_ms);
+
+/* Row slab of `rank` on a level with N elements per side, for a finest grid
+ * n_elem = n_coarse * 2^k split over nranks with the given agglom_rows: node rows
+ * [*r0, *r1) on distributed levels (*distributed = 1), or [0, N+1) on replicated
+ * ones (*distributed = 0).  Pure function, no GPU needed. */
+int svk_partition(int32_t n_elem, int32_t n_coarse, int32_t nranks, int32_t rank, int32_t agglom_rows, int32_t N,
+                  int32_t* r0, int32_t* r1, int32_t* distributed);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast the bytes
+ * into svk_config.nccl_id on every rank).  SVK_ERR_NCCL if NCCL cannot be loaded. */
+int svk_nccl_unique_id(uint8_t* out);
+
+/* Distributed mode: make every rank's copy of a finest-level vector complete
+ * (the owned rows of all ranks, all-reduced).  No-op on a single rank. */
+int svk_allgather(svk_ctx* ctx, double* v, void* stream);
 
 const char* svk_status_string(int status);
 const char* svk_last_error(const svk_ctx* ctx);

@@ -1,0 +1,240 @@
+// dist.cuh -- multi-GPU plumbing of libsvk (not in the paper).
+//
+// Row slabs: on the distributed levels (node rows per rank >= agglom_rows) rank
+// r owns node rows [r0, r1) and lattice rows [2 r0, min(2 r1, 2N+1)); slabs are
+// nested across levels (r0 doubles from one level to the next finer one).  The
+// coarser levels are replicated: every rank runs them redundantly after an
+// all-gather of the restricted residual.  Vectors keep the full-size pitched
+// layout on every rank; only the owned rows (plus a halo of 3 node rows per
+// side, refreshed by `exchange`) are meaningful.
+//
+// Transports:
+//  * NcclTransport -- NCCL (loaded with dlopen, so libsvk has no link-time NCCL
+//    dependency): grouped ncclSend/ncclRecv with the two neighbours for halos,
+//    ncclAllReduce (fp64 sum) for dot products and the all-gather.
+//  * EmulTransport -- p logical ranks of one process on one GPU (one host
+//    thread per rank): the same operations through a shared group object,
+//    device-to-device copies and a host barrier.  Test mode only.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace svk {
+
+// node-row slab of `rank` on a level with N elements, given the coarsest
+// distributed level's N (Nla): rows scale by N / Nla so slabs nest.
+inline void slab_rows(int N, int Nla, int nranks, int rank, int* r0, int* r1) {
+  const int64_t s = N / Nla;
+  *r0 = (int)(((int64_t)rank * Nla / nranks) * s);
+  *r1 = rank == nranks - 1 ? N + 1 : (int)(((int64_t)(rank + 1) * Nla / nranks) * s);
+}
+
+// A contiguous block of doubles to send / receive.
+struct Block {
+  double* ptr;
+  int64_t count;
+};
+
+class Transport {
+ public:
+  virtual ~Transport() {}
+  // send lo_send to rank-1 and hi_send to rank+1; receive lo_recv from rank-1 and
+  // hi_recv from rank+1 (blocks of a side are absent at the domain edges)
+  virtual int exchange(const std::vector<Block>& lo_send, const std::vector<Block>& lo_recv,
+                       const std::vector<Block>& hi_send, const std::vector<Block>& hi_recv, cudaStream_t s,
+                       std::string& err) = 0;
+  virtual int allreduce_sum(double* buf, int64_t count, cudaStream_t s, std::string& err) = 0;
+};
+
+// ----------------------------------------------------------------- NCCL
+typedef int ncclResult_t_;
+typedef void* ncclComm_t_;
+struct NcclId {
+  char internal[128];
+};
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t_ (*GetUniqueId)(NcclId*) = nullptr;
+  ncclResult_t_ (*CommInitRank)(ncclComm_t_*, int, NcclId, int) = nullptr;
+  ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
+  ncclResult_t_ (*Send)(const void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*Recv)(void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*GroupStart)() = nullptr;
+  ncclResult_t_ (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+  bool ok() const { return h && GetUniqueId && CommInitRank && Send && Recv && AllReduce && GroupStart && GroupEnd; }
+};
+inline NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+    api.Send = (decltype(api.Send))dlsym(api.h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+  });
+  return api;
+}
+constexpr int kNcclDouble = 8, kNcclSum = 0;  // ncclFloat64, ncclSum
+
+class NcclTransport : public Transport {
+ public:
+  NcclTransport(int rank, int nranks) : rank_(rank), nranks_(nranks) {}
+  ~NcclTransport() override {
+    if (comm_ && nccl_api().CommDestroy) nccl_api().CommDestroy(comm_);
+  }
+  int init(const uint8_t id[128], std::string& err) {
+    NcclApi& a = nccl_api();
+    if (!a.ok()) {
+      err = "NCCL (libnccl.so.2) could not be loaded";
+      return -1;
+    }
+    NcclId nid;
+    std::memcpy(nid.internal, id, 128);
+    const int r = a.CommInitRank(&comm_, nranks_, nid, rank_);
+    if (r != 0) {
+      err = std::string("ncclCommInitRank: ") + (a.GetErrorString ? a.GetErrorString(r) : "error");
+      return -1;
+    }
+    return 0;
+  }
+  int exchange(const std::vector<Block>& lo_send, const std::vector<Block>& lo_recv, const std::vector<Block>& hi_send,
+               const std::vector<Block>& hi_recv, cudaStream_t s, std::string& err) override {
+    NcclApi& a = nccl_api();
+    int r = a.GroupStart();
+    for (const Block& b : lo_send)
+      if (!r && b.count) r = a.Send(b.ptr, b.count, kNcclDouble, rank_ - 1, comm_, s);
+    for (const Block& b : lo_recv)
+      if (!r && b.count) r = a.Recv(b.ptr, b.count, kNcclDouble, rank_ - 1, comm_, s);
+    for (const Block& b : hi_send)
+      if (!r && b.count) r = a.Send(b.ptr, b.count, kNcclDouble, rank_ + 1, comm_, s);
+    for (const Block& b : hi_recv)
+      if (!r && b.count) r = a.Recv(b.ptr, b.count, kNcclDouble, rank_ + 1, comm_, s);
+    const int r2 = a.GroupEnd();
+    if (r || r2) {
+      err = "NCCL halo exchange failed";
+      return -1;
+    }
+    return 0;
+  }
+  int allreduce_sum(double* buf, int64_t count, cudaStream_t s, std::string& err) override {
+    if (nccl_api().AllReduce(buf, buf, (size_t)count, kNcclDouble, kNcclSum, comm_, s) != 0) {
+      err = "ncclAllReduce failed";
+      return -1;
+    }
+    return 0;
+  }
+
+ private:
+  int rank_, nranks_;
+  ncclComm_t_ comm_ = nullptr;
+};
+
+// ----------------------------------------------------------------- emulation
+// p logical ranks in one process (one host thread each) on one device.
+struct EmulGroup {
+  int nranks;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  // per-rank slots for the current collective
+  std::vector<std::vector<Block>> lo_send, hi_send;
+  std::vector<std::vector<double>> red;
+  explicit EmulGroup(int n) : nranks(n), lo_send(n), hi_send(n), red(n) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+inline std::mutex& emul_registry_mu() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<int, std::weak_ptr<EmulGroup>>& emul_registry() {
+  static std::map<int, std::weak_ptr<EmulGroup>> r;
+  return r;
+}
+
+class EmulTransport : public Transport {
+ public:
+  EmulTransport(int rank, int nranks, int key) : rank_(rank) {
+    std::lock_guard<std::mutex> lk(emul_registry_mu());
+    auto& w = emul_registry()[key];
+    group_ = w.lock();
+    if (!group_) {
+      group_ = std::make_shared<EmulGroup>(nranks);
+      w = group_;
+    }
+  }
+  int exchange(const std::vector<Block>& lo_send, const std::vector<Block>& lo_recv, const std::vector<Block>& hi_send,
+               const std::vector<Block>& hi_recv, cudaStream_t s, std::string& err) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      err = "emulated exchange: stream sync failed";
+      return -1;
+    }
+    EmulGroup& G = *group_;
+    G.lo_send[rank_] = lo_send;
+    G.hi_send[rank_] = hi_send;
+    G.barrier();
+    // my lo_recv = (rank-1)'s hi_send; my hi_recv = (rank+1)'s lo_send
+    for (size_t k = 0; k < lo_recv.size(); ++k)
+      cudaMemcpy(lo_recv[k].ptr, G.hi_send[rank_ - 1][k].ptr, lo_recv[k].count * sizeof(double),
+                 cudaMemcpyDeviceToDevice);
+    for (size_t k = 0; k < hi_recv.size(); ++k)
+      cudaMemcpy(hi_recv[k].ptr, G.lo_send[rank_ + 1][k].ptr, hi_recv[k].count * sizeof(double),
+                 cudaMemcpyDeviceToDevice);
+    G.barrier();
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
+  int allreduce_sum(double* buf, int64_t count, cudaStream_t s, std::string& err) override {
+    EmulGroup& G = *group_;
+    G.red[rank_].resize(count);
+    if (cudaMemcpyAsync(G.red[rank_].data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      err = "emulated allreduce: copy failed";
+      return -1;
+    }
+    G.barrier();
+    std::vector<double> sum(count, 0.0);
+    for (int r = 0; r < G.nranks; ++r)  // fixed rank order: deterministic
+      for (int64_t i = 0; i < count; ++i) sum[i] += G.red[r][i];
+    G.barrier();
+    cudaMemcpy(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice);
+    return 0;
+  }
+
+ private:
+  int rank_;
+  std::shared_ptr<EmulGroup> group_;
+};
+
+}  // namespace svk

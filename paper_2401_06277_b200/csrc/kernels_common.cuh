@@ -211,12 +211,14 @@ __device__ __forceinline__ int p2col(int c, int* f, double* w) {
   return 5;
 }
 
-// x_f += P e_c on non-Dirichlet fine points (Dirichlet rows of P e_c are 0)
+// x_f += P e_c on non-Dirichlet fine points (Dirichlet rows of P e_c are 0),
+// owned rows of the slab only (lattice rows [2 r0, 2 r1), node rows [r0, r1))
 __global__ void k_prolong_add(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec, double* __restrict__ xf) {
   const int plane = blockIdx.z;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y + (plane < 2 ? 2 * gf.r0 : gf.r0);
   if (plane < 2) {
+    if (j >= 2 * gf.r1) return;
     if (i < 1 || j < 1 || i >= gf.lat - 1 || j >= gf.lat - 1) return;
     int cx[3], cy[3];
     double wx[3], wy[3];
@@ -230,7 +232,7 @@ __global__ void k_prolong_add(LevelGeom gf, LevelGeom gc, const double* __restri
     }
     xf[(plane ? gf.ouy : gf.oux) + (int64_t)j * gf.pu + i] += s;
   } else {
-    if (i > gf.N || j > gf.N) return;
+    if (i > gf.N || j > gf.N || j >= gf.r1) return;
     const int ax = i >> 1, ay = j >> 1;
     const double* e = ec + gc.op;
     double s;

@@ -42,14 +42,14 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   const int xc0 = 2 * kx0 - 6, pc0 = kx0 - 4;
   int spB, spE, Y0 = 0, Y1 = 0, y0 = 0, y1 = 0;
   if (MODE == 0) {
-    y0 = blockIdx.y * R.chunk;
-    y1 = min(y0 + R.chunk, N + 1);
+    y0 = g.r0 + blockIdx.y * R.chunk;
+    y1 = min(y0 + R.chunk, g.r1);
     if (y0 >= y1) return;
     spB = y0 - 1;
     spE = y1 - 1;
   } else {
-    Y0 = blockIdx.y * R.chunk;
-    Y1 = min(Y0 + R.chunk, R.gc.N + 1);
+    Y0 = R.gc.r0 + blockIdx.y * R.chunk;
+    Y1 = min(Y0 + R.chunk, R.gc.r1);
     if (Y0 >= Y1) return;
     spB = 2 * Y0 - 2;
     spE = 2 * Y1;
@@ -190,7 +190,7 @@ inline int launch_residual_strip(const LevelGeom& g, const LevelGeom* gc, const 
   ResidArgs R{g, gc ? *gc : g, 0, out};
   if (!gc) {
     R.chunk = fused_chunk(g, nstrips, nsm);
-    const dim3 grid(nstrips, (g.N + 1 + R.chunk - 1) / R.chunk);
+    const dim3 grid(nstrips, (g.r1 - g.r0 + R.chunk - 1) / R.chunk);
     if (b) k_residual_strip<false, 0><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
     else k_residual_strip<true, 0><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
   } else {
@@ -199,7 +199,7 @@ inline int launch_residual_strip(const LevelGeom& g, const LevelGeom* gc, const 
     const int ncov = (int)std::max<int64_t>(std::max<int64_t>(g.pu / 2, g.pp), gc->pu);
     const int ns = (ncov + fz::kNOUT - 1) / fz::kNOUT;
     R.chunk = std::max(1, fused_chunk(*gc, ns, nsm) / 2 + 1);
-    const dim3 grid(ns, (gc->N + 1 + R.chunk - 1) / R.chunk);
+    const dim3 grid(ns, (gc->r1 - gc->r0 + R.chunk - 1) / R.chunk);
     k_residual_strip<false, 1><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
   }
   return 0;

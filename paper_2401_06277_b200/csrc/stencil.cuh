@@ -43,6 +43,9 @@ struct LevelGeom {
   int64_t oux, ouy, op;  // plane offsets
   int64_t len;    // vector length
   double h;       // 1/N
+  // row slab owned by this rank (node rows [r0, r1); lattice rows [2 r0, min(2 r1, lat))).
+  // Single-GPU / replicated levels own everything: r0 = 0, r1 = N + 1.
+  int r0, r1;
 };
 
 }  // namespace svk

@@ -9,7 +9,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -19,6 +21,7 @@
 #include "krylov.cuh"
 #include "sweep_fused.cuh"
 #include "residual_strip.cuh"
+#include "dist.cuh"
 
 using namespace svk;
 
@@ -45,7 +48,6 @@ struct svk_ctx {
   double* d_w = nullptr;
   double* d_r = nullptr;
   double* d_part = nullptr;
-  double* d_part2 = nullptr;
   double* d_coef = nullptr;
   double* h_pin = nullptr;
   int coef_cap = 0;
@@ -57,6 +59,10 @@ struct svk_ctx {
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;  // pool, used in (start, stop) pairs
   size_t prof_used = 0;
+  // multi-GPU row slabs (dist.cuh): levels la..nlev-1 are distributed
+  std::unique_ptr<Transport> tr;
+  int la = 1 << 30;
+  bool poison = false;  // SVK_POISON_HALO=1: NaN-fill rows beyond the halo after each exchange (tests)
   std::string err;
 };
 
@@ -68,6 +74,14 @@ std::mutex g_tab_mu;
 bool g_tab_done[64] = {false};
 
 int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+
+// first distributed level: the coarsest level l >= 1 with at least agglom_rows
+// node rows per rank; Ns.size() if none
+int first_dist_level(const std::vector<int>& Ns, int nranks, int agglom_rows) {
+  for (int l = 1; l < (int)Ns.size(); ++l)
+    if ((int64_t)Ns[l] >= (int64_t)agglom_rows * nranks) return l;
+  return (int)Ns.size();
+}
 
 LevelGeom make_geom(int N) {
   LevelGeom g{};
@@ -81,6 +95,8 @@ LevelGeom make_geom(int N) {
   g.op = 2 * plane;
   g.len = g.op + round_up((int64_t)(N + 1) * g.pp, 32);
   g.h = 1.0 / N;
+  g.r0 = 0;
+  g.r1 = N + 1;
   return g;
 }
 
@@ -226,13 +242,106 @@ int op_residual(svk_ctx* ctx, int l, const double* x, const double* b, double* r
   return SVK_OK;
 }
 // r_c = P^T (b - A x) on level l-1 in one pass (alg:mg lines 3-4)
+// (coarse rows computed: the halves of this rank's fine slab, so that on the
+// agglomeration level every coarse row is produced by exactly one rank)
 int op_residual_restrict(svk_ctx* ctx, int l, const double* x, const double* b, double* rc, cudaStream_t s) {
-  if (launch_residual_strip(ctx->g[l], &ctx->g[l - 1], ctx->h_fac[l], x, b, rc, ctx->nsm, s) != 0) {
+  const LevelGeom& gf = ctx->g[l];
+  LevelGeom gc = ctx->g[l - 1];
+  gc.r0 = gf.r0 / 2;
+  gc.r1 = gf.r1 == gf.N + 1 ? gc.N + 1 : gf.r1 / 2;
+  if (launch_residual_strip(gf, &gc, ctx->h_fac[l], x, b, rc, ctx->nsm, s) != 0) {
     ctx->err = "residual+restrict: TMA descriptor encoding failed";
     return SVK_ERR_CUDA;
   }
   CKL();
   return SVK_OK;
+}
+
+// ------------------------------------------------------------ multi-GPU plumbing
+constexpr int kHalo = 4;  // node rows of halo per side (2 kHalo lattice rows)
+
+bool dist_level(const svk_ctx* ctx, int l) { return ctx->tr && l >= ctx->la; }
+
+Block plane_rows(double* v, int64_t off, int64_t pitch, int a, int b) {
+  return Block{v + off + (int64_t)a * pitch, (int64_t)std::max(0, b - a) * pitch};
+}
+
+// refresh the halo rows of v on level l from the neighbouring ranks
+int op_halo(svk_ctx* ctx, int l, double* v, cudaStream_t s) {
+  if (!dist_level(ctx, l)) return SVK_OK;
+  const LevelGeom& g = ctx->g[l];
+  const int rank = ctx->cfg.rank, P = ctx->cfg.nranks, lat = g.lat, np = g.N + 1;
+  const int lo = g.r0, hi = g.r1, H = kHalo;
+  std::vector<Block> ls, lr, hs, hr;
+  auto add = [&](std::vector<Block>& dst, int ua, int ub, int pa, int pb) {
+    dst.push_back(plane_rows(v, g.oux, g.pu, ua, ub));
+    dst.push_back(plane_rows(v, g.ouy, g.pu, ua, ub));
+    dst.push_back(plane_rows(v, g.op, g.pp, pa, pb));
+  };
+  if (rank > 0) {
+    add(ls, 2 * lo, std::min(2 * lo + 2 * H, lat), lo, std::min(lo + H, np));
+    add(lr, 2 * lo - 2 * H, 2 * lo, lo - H, lo);
+  }
+  if (rank < P - 1) {
+    add(hs, 2 * hi - 2 * H, 2 * hi, hi - H, hi);
+    add(hr, 2 * hi, std::min(2 * hi + 2 * H, lat), hi, std::min(hi + H, np));
+  }
+  if (ctx->tr->exchange(ls, lr, hs, hr, s, ctx->err) != 0) return SVK_ERR_NCCL;
+  ctx->launches++;
+  if (ctx->poison) {  // rows no kernel may read: NaN (0xFF bytes)
+    const int ua = std::max(0, 2 * lo - 2 * H), ub = std::min(lat, 2 * hi + 2 * H);
+    const int pa = std::max(0, lo - H), pb = std::min(np, hi + H);
+    for (int64_t off : {g.oux, g.ouy}) {
+      CK(cudaMemsetAsync(v + off, 0xFF, (size_t)ua * g.pu * sizeof(double), s));
+      CK(cudaMemsetAsync(v + off + (int64_t)ub * g.pu, 0xFF, (size_t)(lat - ub) * g.pu * sizeof(double), s));
+    }
+    CK(cudaMemsetAsync(v + g.op, 0xFF, (size_t)pa * g.pp * sizeof(double), s));
+    CK(cudaMemsetAsync(v + g.op + (int64_t)pb * g.pp, 0xFF, (size_t)(np - pb) * g.pp * sizeof(double), s));
+  }
+  return SVK_OK;
+}
+
+int op_allreduce(svk_ctx* ctx, double* buf, int64_t count, cudaStream_t s) {
+  if (!ctx->tr) return SVK_OK;
+  if (ctx->tr->allreduce_sum(buf, count, s, ctx->err) != 0) return SVK_ERR_NCCL;
+  ctx->launches++;
+  return SVK_OK;
+}
+
+// zero every entry of v outside this rank's owned rows on level l (and the plane tails)
+int op_zero_unowned(svk_ctx* ctx, int l, double* v, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  const int a = 2 * g.r0, b = std::min(2 * g.r1, g.lat);
+  const int64_t ends[3] = {g.ouy, g.op, g.len};
+  const int64_t offs[3] = {g.oux, g.ouy, g.op};
+  for (int k = 0; k < 3; ++k) {
+    const int64_t pitch = k < 2 ? g.pu : g.pp;
+    const int ra = k < 2 ? a : g.r0, rb = k < 2 ? b : g.r1;
+    CK(cudaMemsetAsync(v + offs[k], 0, (size_t)ra * pitch * sizeof(double), s));
+    const int64_t e = offs[k] + (int64_t)rb * pitch;
+    CK(cudaMemsetAsync(v + e, 0, (size_t)(ends[k] - e) * sizeof(double), s));
+  }
+  return SVK_OK;
+}
+
+// owned index segments of a level-l vector, in double2 units
+Seg3 owned_segments(const svk_ctx* ctx, int l) {
+  const LevelGeom& g = ctx->g[l];
+  Seg3 S{};
+  if (!dist_level(ctx, l)) {
+    const int64_t n2 = g.len / 2;
+    S.cum2[1] = S.cum2[2] = S.cum2[3] = n2;
+    return S;
+  }
+  const int a = 2 * g.r0, b = std::min(2 * g.r1, g.lat);
+  const int64_t nu2 = (int64_t)(b - a) * g.pu / 2, np2 = (int64_t)(g.r1 - g.r0) * g.pp / 2;
+  S.off2[0] = (g.oux + (int64_t)a * g.pu) / 2;
+  S.off2[1] = (g.ouy + (int64_t)a * g.pu) / 2;
+  S.off2[2] = (g.op + (int64_t)g.r0 * g.pp) / 2;
+  S.cum2[1] = nu2;
+  S.cum2[2] = 2 * nu2;
+  S.cum2[3] = 2 * nu2 + np2;
+  return S;
 }
 
 int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero,
@@ -309,53 +418,44 @@ int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
 }
 
 // alg:mg on level l; x in/out; x_zero: x is known to be 0 on entry
+// Distributed levels (row slabs): every operation computes the owned rows; the
+// halos of b (on entry), of x after every relaxation and after the correction,
+// are refreshed by op_halo, so the returned x has valid halos.  On the
+// agglomeration level the restricted residual is assembled on every rank by an
+// all-reduce of the disjoint, zero-padded slab pieces; the coarser levels then
+// run redundantly (replicated) on every rank.
 int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStream_t s) {
   const LevelGeom& g = ctx->g[l];
   if (l == 0) return op_coarse(ctx, b, x, s);
+  const bool D = dist_level(ctx, l);
+  if (D) {
+    TRY(op_halo(ctx, l, const_cast<double*>(b), s));
+    if (!x_zero) TRY(op_halo(ctx, l, x, s));
+  }
   double* cur = x;
   double* oth = ctx->ws_t[l];
   for (int k = 0; k < ctx->cfg.nu_pre; ++k) {  // "Relax on u_l and p_l"
     TRY(op_sweep(ctx, l, cur, b, oth, x_zero && k == 0, s));
     std::swap(cur, oth);
+    if (D) TRY(op_halo(ctx, l, cur, s));
   }
   if (ctx->cfg.nu_pre == 0 && x_zero) CK(cudaMemsetAsync(cur, 0, g.len * sizeof(double), s));
+  const bool agglomerate = D && !dist_level(ctx, l - 1);
+  if (agglomerate) CK(cudaMemsetAsync(ctx->ws_b[l - 1], 0, ctx->g[l - 1].len * sizeof(double), s));
   TRY(op_residual_restrict(ctx, l, cur, b, ctx->ws_b[l - 1], s));  // "Compute residual" + "Restriction"
+  if (agglomerate) TRY(op_allreduce(ctx, ctx->ws_b[l - 1], ctx->g[l - 1].len, s));
   TRY(op_mg(ctx, l - 1, ctx->ws_b[l - 1], ctx->ws_x[l - 1], true, s));  // A_0^{-1} or MG(l-1)
   TRY(op_prolong_add(ctx, l, ctx->ws_x[l - 1], cur, s));       // "Correction"
+  if (D) TRY(op_halo(ctx, l, cur, s));
   for (int k = 0; k < ctx->cfg.nu_post; ++k) {                 // "Relax on u_l and p_l"
     TRY(op_sweep(ctx, l, cur, b, oth, false, s));
     std::swap(cur, oth);
+    if (D) TRY(op_halo(ctx, l, cur, s));
   }
   if (cur != x) CK(cudaMemcpyAsync(x, cur, g.len * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return SVK_OK;
 }
 
-// out[0..m) = V[i]^T w  (deterministic), written to d_coef + off
-int op_dots(svk_ctx* ctx, const std::vector<const double*>& vs, const double* w, int64_t n, int off, cudaStream_t s) {
-  for (size_t g0 = 0; g0 < vs.size(); g0 += kMaxM) {
-    VecPtrs p{};
-    const int m = (int)std::min<size_t>(kMaxM, vs.size() - g0);
-    for (int q = 0; q < m; ++q) p.p[q] = vs[g0 + q];
-    if (m == 1) k_multidot<1><<<kDotBlocks, kRedThreads, 0, s>>>(p, 1, w, n, ctx->d_part);
-    else if (m <= 4) k_multidot<4><<<kDotBlocks, kRedThreads, 0, s>>>(p, m, w, n, ctx->d_part);
-    else k_multidot<8><<<kDotBlocks, kRedThreads, 0, s>>>(p, m, w, n, ctx->d_part);
-    CKL();
-    k_reduce_partials<<<m, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + off + g0, 0);
-    CKL();
-  }
-  return SVK_OK;
-}
-int op_axpys(svk_ctx* ctx, double* w, const std::vector<const double*>& vs, int off, double sign, int64_t n,
-             cudaStream_t s) {
-  for (size_t g0 = 0; g0 < vs.size(); g0 += kMaxM) {
-    VecPtrs p{};
-    const int m = (int)std::min<size_t>(kMaxM, vs.size() - g0);
-    for (int q = 0; q < m; ++q) p.p[q] = vs[g0 + q];
-    k_multiaxpy<<<kDotBlocks, 256, 0, s>>>(w, p, m, ctx->d_coef + off + g0, sign, n);
-    CKL();
-  }
-  return SVK_OK;
-}
 int ensure_coef(svk_ctx* ctx, int need) {
   if (need <= ctx->coef_cap) return SVK_OK;
   int cap = std::max(need, 2 * ctx->coef_cap);
@@ -366,14 +466,6 @@ int ensure_coef(svk_ctx* ctx, int need) {
   ctx->coef_cap = cap;
   return SVK_OK;
 }
-int host_norm(svk_ctx* ctx, const double* v, int64_t n, double* out, cudaStream_t s) {
-  TRY(op_dots(ctx, {v}, v, n, 0, s));
-  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  *out = std::sqrt(ctx->h_pin[0]);
-  return SVK_OK;
-}
-
 // ---------------------------------------------------------------------------
 // Gram-Schmidt passes; basis pointers are passed by value (kernel-parameter space).
 // out[0..m) = V_i . w (deterministic), written to d_coef + off.
@@ -382,27 +474,29 @@ VecList veclist(const double* const* v, int m) {
   for (int i = 0; i < m && i < kCgsMax; ++i) L.p[i] = v[i];
   return L;
 }
-int cgs_dots(svk_ctx* ctx, const double* const* dV, int m, const double* w, int64_t n, int off, cudaStream_t s) {
+// Distributed: the dots run over the owned segments S and are all-reduced.
+int cgs_dots(svk_ctx* ctx, const double* const* dV, int m, const double* w, const Seg3& S, int off, cudaStream_t s) {
   constexpr int kDot = 16;
   for (int c0 = 0; c0 < m; c0 += kDot) {
     const int mm = std::min(kDot, m - c0);
-    if (mm <= 4) k_cgs_dots<4><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
-    else if (mm <= 8) k_cgs_dots<8><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
-    else k_cgs_dots<16><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, n, ctx->d_part);
+    if (mm <= 4) k_cgs_dots<4><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
+    else if (mm <= 8) k_cgs_dots<8><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
+    else k_cgs_dots<16><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
     CKL();
     k_reduce_partials<<<mm, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + off + c0, 0);
     CKL();
   }
+  if (ctx->tr) TRY(op_allreduce(ctx, ctx->d_coef + off, m, s));
   return SVK_OK;
 }
 // w_out = w - sum_i c_i V_i (c at d_coef + coff); squared norm of w_out -> d_coef + noff (if noff >= 0)
 int cgs_update(svk_ctx* ctx, const double* const* dV, int m, int coff, const double* w, double* wout, int64_t n,
-               int noff, cudaStream_t s) {
+               const Seg3& S, int noff, cudaStream_t s) {
   const double* src = w;
   if (m == 0 && w != wout) CK(cudaMemcpyAsync(wout, w, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   for (int c0 = 0; c0 < m; c0 += kCgsMax) {
     const int mm = std::min(kCgsMax, m - c0);
-    k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, ctx->d_coef + coff + c0, src, wout, n,
+    k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, ctx->d_coef + coff + c0, src, wout, S,
                                                      ctx->d_part);
     CKL();
     src = wout;
@@ -410,7 +504,16 @@ int cgs_update(svk_ctx* ctx, const double* const* dV, int m, int coff, const dou
   if (noff >= 0) {
     k_reduce_partials<<<1, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + noff, 0);
     CKL();
+    if (ctx->tr) TRY(op_allreduce(ctx, ctx->d_coef + noff, 1, s));
   }
+  return SVK_OK;
+}
+// |v| on the host (owned segments, all-reduced)
+int host_norm(svk_ctx* ctx, const double* v, const Seg3& S, double* out, cudaStream_t s) {
+  TRY(cgs_dots(ctx, &v, 1, v, S, 0, s));
+  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *out = std::sqrt(std::max(ctx->h_pin[0], 0.0));
   return SVK_OK;
 }
 
@@ -427,6 +530,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   const int L = ctx->nlev - 1;
   const LevelGeom& g = ctx->g[L];
   const int64_t n = g.len;
+  const Seg3 S = owned_segments(ctx, L);
   svk_report R{};
   double tv = 0, to = 0;
   // coefficient area: [c1 (maxit+1) | c2 (maxit+1) | raw (maxit+1) | nrm | n^-2 (maxit+1)]
@@ -444,8 +548,9 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   };
   TRY(ensure_vec(ctx->V, 0));
   // V~_0 = r0 = b - A x0, n_0 = |r0|
+  TRY(op_halo(ctx, L, x, s));
   TRY(op_residual(ctx, L, x, b, ctx->V[0], s));
-  TRY(cgs_dots(ctx, (const double* const*)ctx->V.data(), 1, ctx->V[0], n, onrm, s));
+  TRY(cgs_dots(ctx, (const double* const*)ctx->V.data(), 1, ctx->V[0], S, onrm, s));
   CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef + onrm, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const double beta = std::sqrt(std::max(ctx->h_pin[0], 0.0));
@@ -477,14 +582,14 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       CK(cudaEventRecord(ctx->ev[1], s));
       // w~ = A z~_j ; CGS2 against V~_0..V~_j ; |w~''|
       TRY(op_residual(ctx, L, ctx->Z[j], nullptr, ctx->d_w, s));
-      TRY(cgs_dots(ctx, hV, m, ctx->d_w, n, oraw, s));
+      TRY(cgs_dots(ctx, hV, m, ctx->d_w, S, oraw, s));
       k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
       CKL();
-      TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->d_w, n, -1, s));
-      TRY(cgs_dots(ctx, hV, m, ctx->d_w, n, oraw, s));
+      TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->d_w, n, S, -1, s));
+      TRY(cgs_dots(ctx, hV, m, ctx->d_w, S, oraw, s));
       k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
       CKL();
-      TRY(cgs_update(ctx, hV, m, o2, ctx->d_w, ctx->V[j + 1], n, onrm, s));
+      TRY(cgs_update(ctx, hV, m, o2, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
       CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -537,15 +642,16 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       for (int c0 = 0; c0 < k; c0 += kCgsMax) {
         const int mm = std::min(kCgsMax, k - c0);
         k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist((const double* const*)ctx->Z.data() + c0, mm), mm,
-                                                         ctx->d_coef + o1 + c0, x, x, n, ctx->d_part);
+                                                         ctx->d_coef + o1 + c0, x, x, S, ctx->d_part);
         CKL();
       }
     }
   }
   double rn = 0.0;
   if (beta > 0) {
+    TRY(op_halo(ctx, L, x, s));
     TRY(op_residual(ctx, L, x, b, ctx->d_r, s));
-    TRY(host_norm(ctx, ctx->d_r, n, &rn, s));
+    TRY(host_norm(ctx, ctx->d_r, S, &rn, s));
   }
   R.iterations = k;
   R.converged = conv ? 1 : 0;
@@ -579,7 +685,6 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_w);
   F(ctx->d_r);
   F(ctx->d_part);
-  F(ctx->d_part2);
   F(ctx->d_coef);
   F(ctx->d_hb);
   F(ctx->d_hx);
@@ -612,6 +717,24 @@ int create_impl(svk_ctx* ctx) {
   for (int N = c.n_coarse; N <= c.n_elem; N *= 2) Ns.push_back(N);
   ctx->nlev = (int)Ns.size();
   for (int N : Ns) ctx->g.push_back(make_geom(N));
+  // row slabs (dist.cuh).  Without a distributed level every rank runs the whole
+  // problem redundantly and no transport is created.
+  if (c.nranks > 1) {
+    ctx->la = first_dist_level(Ns, c.nranks, c.agglom_rows);
+    if (ctx->la < ctx->nlev) {
+      for (int l = ctx->la; l < ctx->nlev; ++l)
+        slab_rows(Ns[l], Ns[ctx->la], c.nranks, c.rank, &ctx->g[l].r0, &ctx->g[l].r1);
+      if (c.transport == SVK_TRANSPORT_NCCL) {
+        auto* t = new NcclTransport(c.rank, c.nranks);
+        ctx->tr.reset(t);
+        if (t->init(c.nccl_id, ctx->err) != 0) return SVK_ERR_NCCL;
+      } else {
+        ctx->tr.reset(new EmulTransport(c.rank, c.nranks, c.emul_group));
+      }
+    }
+    const char* pz = std::getenv("SVK_POISON_HALO");
+    ctx->poison = pz && pz[0] == '1';
+  }
   CK(cudaMalloc(&ctx->d_Ns, Ns.size() * sizeof(int)));
   CK(cudaMemcpy(ctx->d_Ns, Ns.data(), Ns.size() * sizeof(int), cudaMemcpyHostToDevice));
   for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ctx->ev[k]));
@@ -678,7 +801,6 @@ int create_impl(svk_ctx* ctx) {
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
   }
   CK(cudaMalloc(&ctx->d_part, (size_t)(kCgsMax + 1) * kDotBlocks * sizeof(double)));
-  CK(cudaMalloc(&ctx->d_part2, (size_t)(kCgsMax + 1) * sizeof(double)));
   CK(cudaDeviceSynchronize());
   return SVK_OK;
 }
@@ -703,6 +825,10 @@ int svk_config_default(svk_config* cfg, int32_t n_elem) {
   cfg->coarse = SVK_COARSE_EXACT;
   cfg->sweep_impl = SVK_SWEEP_FUSED;
   cfg->device = 0;
+  cfg->rank = 0;
+  cfg->nranks = 1;
+  cfg->transport = SVK_TRANSPORT_NONE;
+  cfg->agglom_rows = 64;
   return SVK_OK;
 }
 
@@ -719,6 +845,10 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
     n /= 2;
   }
   if (n != cfg->n_coarse) return SVK_ERR_INVALID;
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return SVK_ERR_INVALID;
+  if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
+                          (cfg->transport != SVK_TRANSPORT_NCCL && cfg->transport != SVK_TRANSPORT_EMULATED)))
+    return SVK_ERR_INVALID;
   svk_ctx* ctx = new svk_ctx;
   ctx->cfg = *cfg;
   int st = create_impl(ctx);
@@ -757,6 +887,10 @@ int svk_level_info(const svk_ctx* ctx, int32_t level, svk_level* out) {
   out->pitch_p = g.pp;
   out->n_dof = 2 * (int64_t)g.lat * g.lat + (int64_t)(g.N + 1) * (g.N + 1);
   out->n_patch = (int64_t)(g.N + 1) * (g.N + 1);
+  out->row0 = g.r0;
+  out->row1 = g.r1;
+  out->distributed = dist_level(ctx, level) ? 1 : 0;
+  out->halo_rows = out->distributed ? kHalo : 0;
   return SVK_OK;
 }
 
@@ -779,6 +913,7 @@ int svk_residual(svk_ctx* ctx, int32_t level, const double* x, const double* b, 
   TRY(valid_ptr(ctx, x, "x"));
   TRY(valid_ptr(ctx, b, "b"));
   TRY(valid_ptr(ctx, r, "r"));
+  TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
   return op_residual(ctx, level, x, b, r, (cudaStream_t)stream);
 }
 
@@ -786,6 +921,7 @@ int svk_matvec(svk_ctx* ctx, int32_t level, const double* x, double* y, void* st
   TRY(valid_level(ctx, level));
   TRY(valid_ptr(ctx, x, "x"));
   TRY(valid_ptr(ctx, y, "y"));
+  TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
   return op_residual(ctx, level, x, nullptr, y, (cudaStream_t)stream);
 }
 
@@ -802,6 +938,8 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
   cudaStream_t s = (cudaStream_t)stream;
   const LevelGeom& g = ctx->g[level];
   if (ctx->cfg.sweep_impl == SVK_SWEEP_UNFUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
+  TRY(op_halo(ctx, level, const_cast<double*>(b), s));
+  TRY(op_halo(ctx, level, const_cast<double*>(x_in), s));
   if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);
   if (!ctx->d_sw) TRY(alloc_vec(ctx, &ctx->d_sw, ctx->g.back().len));
   // ping-pong so that the last sweep lands in x_out
@@ -809,6 +947,7 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
   int dst = (nsweeps % 2 == 1) ? 0 : 1;
   const double* cur = x_in;
   for (int k = 0; k < nsweeps; ++k) {
+    if (k > 0) TRY(op_halo(ctx, level, const_cast<double*>(cur), s));
     TRY(op_sweep(ctx, level, cur, b, bufs[dst], false, s));
     cur = bufs[dst];
     dst ^= 1;
@@ -875,6 +1014,10 @@ int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, do
   }
   int st = fgmres_impl(ctx, ctx->d_hb, ctx->d_hx, rtol, maxit, nullptr, rep, s);
   if (st < 0) return st;
+  if (ctx->tr) {  // assemble the full solution on every rank
+    TRY(op_zero_unowned(ctx, ctx->nlev - 1, ctx->d_hx, s));
+    TRY(op_allreduce(ctx, ctx->d_hx, g.len, s));
+  }
   CK(cudaMemcpy2DAsync(x_host, wu, ctx->d_hx + g.oux, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpy2DAsync(x_host + nv, wu, ctx->d_hx + g.ouy, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpy2DAsync(x_host + 2 * nv, wp, ctx->d_hx + g.op, g.pp * sizeof(double), wp, g.N + 1,
@@ -928,6 +1071,49 @@ int svk_sweep_stats(svk_ctx* ctx, int64_t* count, double* total_ms) {
   *total_ms = t;
   ctx->prof_used = 0;
   return SVK_OK;
+}
+
+int svk_partition(int32_t n_elem, int32_t n_coarse, int32_t nranks, int32_t rank, int32_t agglom_rows, int32_t N,
+                  int32_t* r0, int32_t* r1, int32_t* distributed) {
+  if (!r0 || !r1 || !distributed || n_coarse < 4 || n_elem < n_coarse || nranks < 1 || rank < 0 || rank >= nranks ||
+      agglom_rows < kHalo)
+    return SVK_ERR_INVALID;
+  std::vector<int> Ns;
+  for (int64_t m = n_coarse; m <= n_elem; m *= 2) Ns.push_back((int)m);
+  if (Ns.back() != n_elem) return SVK_ERR_INVALID;
+  int l = -1;
+  for (int k = 0; k < (int)Ns.size(); ++k)
+    if (Ns[k] == N) l = k;
+  if (l < 0) return SVK_ERR_INVALID;
+  const int la = nranks > 1 ? first_dist_level(Ns, nranks, agglom_rows) : (int)Ns.size();
+  if (l >= la) {
+    slab_rows(N, Ns[la], nranks, rank, r0, r1);
+    *distributed = 1;
+  } else {
+    *r0 = 0;
+    *r1 = N + 1;
+    *distributed = 0;
+  }
+  return SVK_OK;
+}
+
+int svk_nccl_unique_id(uint8_t* out) {
+  if (!out) return SVK_ERR_INVALID;
+  NcclApi& a = nccl_api();
+  if (!a.ok()) return SVK_ERR_NCCL;
+  NcclId id;
+  if (a.GetUniqueId(&id) != 0) return SVK_ERR_NCCL;
+  std::memcpy(out, id.internal, 128);
+  return SVK_OK;
+}
+
+int svk_allgather(svk_ctx* ctx, double* v, void* stream) {
+  if (!ctx) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, v, "v"));
+  if (!ctx->tr) return SVK_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(op_zero_unowned(ctx, ctx->nlev - 1, v, s));
+  return op_allreduce(ctx, v, ctx->g.back().len, s);
 }
 
 const char* svk_status_string(int status) {

@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu,
     kx = c <= 1 ? c : c + N - 3;
     ky = 2 + (int)(q % (N - 3));
   }
+  if (ky < g.r0 - 1 || ky > g.r1) return;  // patch rows a slab's sweep uses: r0-1 .. r1
   __shared__ double rv[kSlots];
   const int s = threadIdx.x;
   if (s < kSlots) {
@@ -584,8 +585,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   const int N = g.N, lat = g.lat;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int kx0 = blockIdx.x * fz::kNOUT;
-  const int y0 = blockIdx.y * A.chunk;
-  const int y1 = min(y0 + A.chunk, N + 1);
+  const int y0 = g.r0 + blockIdx.y * A.chunk;
+  const int y1 = min(y0 + A.chunk, g.r1);
   if (y0 >= y1) return;
   const int xc0 = 2 * kx0 - 6, pc0 = kx0 - 4;
   const int sB = y0 - 1, sE = y1;
@@ -755,14 +756,15 @@ inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const doubl
 
 // chunk height: about `waves` full waves of 2 CTAs per SM over the strips
 inline int fused_chunk(const LevelGeom& g, int nstrips, int nsm) {
+  const int rows = g.r1 - g.r0;
   const int resident = 2 * nsm;
-  const double work = (double)nstrips * (g.N + 1) / 128.0;
+  const double work = (double)nstrips * rows / 128.0;
   int waves = (int)(work / resident + 0.5);
   if (waves < 1) waves = 1;
   int chunks = (resident * waves) / nstrips;
   if (chunks < 1) chunks = 1;
-  if (chunks > g.N + 1) chunks = g.N + 1;
-  return (g.N + 1 + chunks - 1) / chunks;
+  if (chunks > rows) chunks = rows;
+  return (rows + chunks - 1) / chunks;
 }
 
 // ---- host: TMA descriptors --------------------------------------------------
@@ -825,7 +827,7 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   std::memset(&M, 0, sizeof(M));
   if (!make_vel_map(&M.bv, g, b) || !make_p_map(&M.bp, g, b, fz::PWID)) return -2;
   if (xin && (!make_vel_map(&M.xv, g, xin) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
-  const dim3 grid(nstrips, (g.N + 1 + A.chunk - 1) / A.chunk);
+  const dim3 grid(nstrips, (g.r1 - g.r0 + A.chunk - 1) / A.chunk);
   if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
   else k_vanka_fused<true><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
   return 0;

@@ -21,6 +21,7 @@ PROBLEMS = {"zero": 0, "mms_paper": 1, "mms_inspace": 2, "cavity": 3}
 WEIGHTING = {"mult": 0, "scalar": 1}
 COARSE = {"exact": 0, "sweeps3": 1}
 SWEEP = {"fused": 0, "unfused": 1}
+TRANSPORT = {"none": 0, "nccl": 1, "emulated": 2}
 
 
 class SvkError(RuntimeError):
@@ -30,13 +31,16 @@ class SvkError(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("n_elem", C.c_int32), ("n_coarse", C.c_int32), ("nu", C.c_double), ("omega_v", C.c_double),
                 ("weighting", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("coarse", C.c_int32),
-                ("sweep_impl", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32 * 8)]
+                ("sweep_impl", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("transport", C.c_int32), ("agglom_rows", C.c_int32), ("emul_group", C.c_int32),
+                ("reserved", C.c_int32 * 3), ("nccl_id", C.c_uint8 * 128)]
 
 
 class LevelInfo(C.Structure):
     _fields_ = [("N", C.c_int32), ("lat", C.c_int32), ("vec_len", C.c_int64), ("off_ux", C.c_int64),
                 ("off_uy", C.c_int64), ("off_p", C.c_int64), ("pitch_u", C.c_int64), ("pitch_p", C.c_int64),
-                ("n_dof", C.c_int64), ("n_patch", C.c_int64)]
+                ("n_dof", C.c_int64), ("n_patch", C.c_int64), ("row0", C.c_int32), ("row1", C.c_int32),
+                ("distributed", C.c_int32), ("halo_rows", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -73,6 +77,10 @@ EXPORTS = {
     "svk_launch_count": (C.c_int64, [C.c_void_p]),
     "svk_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "svk_sweep_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
+    "svk_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "svk_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "svk_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_status_string": (C.c_char_p, [C.c_int]),
     "svk_last_error": (C.c_char_p, [C.c_void_p]),
 }
@@ -94,6 +102,38 @@ def load_library(path: str = LIB_PATH):
     return lib
 
 
+def partition(n_elem: int, n_coarse: int, nranks: int, rank: int, agglom_rows: int, N: int):
+    """Node-row slab (r0, r1, distributed) of `rank` on the level with N elements (svk_partition)."""
+    lib = load_library()
+    r0, r1, d = C.c_int32(), C.c_int32(), C.c_int32()
+    st = lib.svk_partition(n_elem, n_coarse, nranks, rank, agglom_rows, N, C.byref(r0), C.byref(r1), C.byref(d))
+    if st != SVK_OK:
+        raise SvkError("svk_partition: %s" % lib.svk_status_string(st).decode())
+    return r0.value, r1.value, bool(d.value)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes); call on rank 0 only."""
+    lib = load_library()
+    buf = (C.c_uint8 * 128)()
+    st = lib.svk_nccl_unique_id(buf)
+    if st != SVK_OK:
+        raise SvkError("svk_nccl_unique_id: %s" % lib.svk_status_string(st).decode())
+    return bytes(buf)
+
+
+def nccl_id_broadcast(group=None, make_id=None) -> bytes:
+    """Rank 0 creates the NCCL id and torch.distributed broadcasts it to every rank
+    (any backend; the bootstrap is host-side plumbing, the solver's traffic is NCCL)."""
+    import torch.distributed as dist
+    make_id = nccl_unique_id if make_id is None else make_id
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if not isinstance(obj[0], (bytes, bytearray)) or len(obj[0]) != 128:
+        raise SvkError("bad NCCL id broadcast")
+    return bytes(obj[0])
+
+
 def _stream(torch):
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -103,7 +143,11 @@ class Solver:
 
     def __init__(self, n_elem: int, n_coarse: int = 4, nu: float = 1.0, omega: float = 0.8,
                  weighting: str = "mult", nu_pre: int = 1, nu_post: int = 1, coarse: str = "exact",
-                 sweep: str = "fused", device: int = 0):
+                 sweep: str = "fused", device: int = 0, rank: int = 0, nranks: int = 1,
+                 transport: str = "none", agglom_rows: int = 64, emul_group: int = 0, nccl_id: bytes | None = None):
+        """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
+        `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
+        "emulated" runs nranks logical ranks of one process on one device (one thread each)."""
         import torch
         if not torch.cuda.is_available():
             raise SvkError("libsvk needs a CUDA device (B200, sm_100a); none is visible")
@@ -114,6 +158,13 @@ class Solver:
         cfg.n_coarse, cfg.nu, cfg.omega_v = n_coarse, nu, omega
         cfg.weighting, cfg.nu_pre, cfg.nu_post = WEIGHTING[weighting], nu_pre, nu_post
         cfg.coarse, cfg.sweep_impl, cfg.device = COARSE[coarse], SWEEP[sweep], device
+        cfg.rank, cfg.nranks, cfg.transport = rank, nranks, TRANSPORT[transport]
+        cfg.agglom_rows, cfg.emul_group = agglom_rows, emul_group
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise SvkError("nccl_id must be 128 bytes")
+            C.memmove(cfg.nccl_id, bytes(nccl_id), 128)
+        self.rank, self.nranks = rank, nranks
         self.cfg = cfg
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -263,6 +314,16 @@ class Solver:
         d = rep.as_dict()
         d["status"] = st
         return x_host, d
+
+    def allgather(self, v):
+        """Distributed mode: complete every rank's copy of a finest-level vector (in place)."""
+        self._chk(self.lib.svk_allgather(self._h, self._vec(v, self.fine, "v"), _stream(self.torch)))
+        return v
+
+    def owned_rows(self, level: int | None = None):
+        """(row0, row1, distributed) node-row slab of this rank on a level."""
+        li = self.info[self.fine if level is None else level]
+        return li.row0, li.row1, bool(li.distributed)
 
     def patch_inverse(self, level: int, cat_x: int, cat_y: int) -> np.ndarray:
         out = np.zeros(51 * 51)
