@@ -48,7 +48,7 @@
  * MULTI-GPU (nranks > 1).  Every rank creates one context with the same
  * configuration except `rank`.  The finest levels are split into row slabs;
  * every call then computes only the rank's owned rows, and the library refreshes
- * halo rows (3 node rows per side) of its input vectors itself, so rows outside
+ * halo rows (4 node rows per side) of its input vectors itself, so rows outside
  * a rank's slab are library-managed scratch.  svk_fgmres / svk_vcycle /
  * svk_vanka_sweep / svk_residual / svk_matvec must be called by all ranks
  * together (they communicate).  svk_allgather assembles a full vector.
@@ -117,7 +117,8 @@ typedef struct svk_config {
   int32_t agglom_rows; /* levels with fewer than agglom_rows node rows per rank are
                           replicated on every rank (coarse agglomeration); default 64, >= 4 */
   int32_t emul_group;  /* EMULATED transport: id of the in-process group to join */
-  int32_t reserved[3];
+  int32_t orth;        /* enum svk_orth: FGMRES Gram-Schmidt; default ADAPTIVE */
+  int32_t reserved[2];
   uint8_t nccl_id[128]; /* NCCL transport: ncclUniqueId from svk_nccl_unique_id() on rank 0,
                            broadcast to every rank by the caller */
 } svk_config;
@@ -129,6 +130,13 @@ typedef struct svk_config {
  * EMULATED -- nranks logical ranks inside ONE process on one device, one host
  *             thread per rank (test mode; same partition, halos and reductions). */
 enum svk_transport { SVK_TRANSPORT_NONE = 0, SVK_TRANSPORT_NCCL = 1, SVK_TRANSPORT_EMULATED = 2 };
+
+/* Arnoldi orthogonalisation of svk_fgmres (the paper does not fix it):
+ * CGS2     -- classical Gram-Schmidt, always two passes ("twice is enough");
+ * ADAPTIVE -- one classical pass; a second pass only when the pass cancelled
+ *             more than a factor kappa = 10 of the vector's norm
+ *             (||w'|| < ||w|| / kappa, a DGKS-type test; reading 18). */
+enum svk_orth { SVK_ORTH_ADAPTIVE = 0, SVK_ORTH_CGS2 = 1 };
 
 typedef struct svk_level {
   int32_t N;          /* elements per side on this level */
@@ -148,7 +156,7 @@ typedef struct svk_report {
   int32_t iterations;      /* FGMRES iterations (= preconditioner applications) */
   int32_t converged;       /* 1 if estimate <= rtol */
   int32_t status;          /* same as the return value */
-  int32_t reserved;
+  int32_t n_reorth;        /* iterations that needed a second Gram-Schmidt pass */
   double rel_residual;     /* true ||b - A x|| / ||b - A x0||, recomputed at exit */
   double t_total_s;        /* wall time of the call (host clock) */
   double t_vcycle_s;       /* device time in V-cycles (CUDA events) */

@@ -53,7 +53,7 @@ struct svk_ctx {
   int coef_cap = 0;
   double* d_hb = nullptr;  // e2e staging
   double* d_hx = nullptr;
-  cudaEvent_t ev[4]{};
+  cudaEvent_t ev[6]{};
   int64_t launches = 0;
   // sweep profiling (svk_set_profiling / svk_sweep_stats)
   bool prof = false;
@@ -69,6 +69,7 @@ struct svk_ctx {
 namespace {
 
 constexpr int kDotBlocks = 148 * 4;
+constexpr double kReorthKappa = 10.0;  // ADAPTIVE orthogonalisation: re-orthogonalise if |w'| < |w| / kappa
 
 std::mutex g_tab_mu;
 bool g_tab_done[64] = {false};
@@ -559,7 +560,8 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
     ctx->err = "non-finite initial residual";
     return SVK_ERR_NONFINITE;
   }
-  int status = SVK_OK, k = 0;
+  int status = SVK_OK, k = 0, n_reorth = 0;
+  std::vector<const double*> dlist;
   bool conv = beta == 0.0;
   std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), gv(maxit + 1, 0.0), nv(maxit + 2);
   std::vector<double> inv_nsq(maxit + 1);
@@ -580,16 +582,15 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       CK(cudaEventRecord(ctx->ev[0], s));
       TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
       CK(cudaEventRecord(ctx->ev[1], s));
-      // w~ = A z~_j ; CGS2 against V~_0..V~_j ; |w~''|
+      // w~ = A z~_j ; classical Gram-Schmidt pass against V~_0..V~_j (its dot
+      // pass also yields |w~|^2) ; V~_j+1 = w~' with |w~'|
       TRY(op_residual(ctx, L, ctx->Z[j], nullptr, ctx->d_w, s));
-      TRY(cgs_dots(ctx, hV, m, ctx->d_w, S, oraw, s));
+      dlist.assign(hV, hV + m);
+      dlist.push_back(ctx->d_w);
+      TRY(cgs_dots(ctx, dlist.data(), m + 1, ctx->d_w, S, oraw, s));
       k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
       CKL();
-      TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->d_w, n, S, -1, s));
-      TRY(cgs_dots(ctx, hV, m, ctx->d_w, S, oraw, s));
-      k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
-      CKL();
-      TRY(cgs_update(ctx, hV, m, o2, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
+      TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
       CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -598,6 +599,24 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       cudaEventElapsedTime(&a12, ctx->ev[1], ctx->ev[2]);
       tv += a01 * 1e-3;
       to += a12 * 1e-3;
+      // second pass: always (CGS2) or when the first pass cancelled more than kappa (DGKS-type test)
+      const double wn2 = ctx->h_pin[oraw + m], wp2 = ctx->h_pin[onrm];
+      if (ctx->cfg.orth == SVK_ORTH_CGS2 || !(wp2 * kReorthKappa * kReorthKappa >= wn2)) {
+        CK(cudaEventRecord(ctx->ev[3], s));
+        TRY(cgs_dots(ctx, hV, m, ctx->V[j + 1], S, oraw, s));
+        k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
+        CKL();
+        TRY(cgs_update(ctx, hV, m, o2, ctx->V[j + 1], ctx->V[j + 1], n, S, onrm, s));
+        CK(cudaEventRecord(ctx->ev[4], s));
+        CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float a34 = 0;
+        cudaEventElapsedTime(&a34, ctx->ev[3], ctx->ev[4]);
+        to += a34 * 1e-3;
+        ++n_reorth;
+      } else {
+        for (int i = 0; i < m; ++i) ctx->h_pin[o2 + i] = 0.0;
+      }
       for (int i = 0; i <= j; ++i) Hij(i, j) = (ctx->h_pin[o1 + i] + ctx->h_pin[o2 + i]) * nv[i] / nv[j];
       const double nn = std::sqrt(std::max(ctx->h_pin[onrm], 0.0));
       const double hn = nn / nv[j];
@@ -654,6 +673,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
     TRY(host_norm(ctx, ctx->d_r, S, &rn, s));
   }
   R.iterations = k;
+  R.n_reorth = n_reorth;
   R.converged = conv ? 1 : 0;
   R.rel_residual = beta > 0 ? rn / beta : 0.0;
   R.t_vcycle_s = tv;
@@ -737,7 +757,7 @@ int create_impl(svk_ctx* ctx) {
   }
   CK(cudaMalloc(&ctx->d_Ns, Ns.size() * sizeof(int)));
   CK(cudaMemcpy(ctx->d_Ns, Ns.data(), Ns.size() * sizeof(int), cudaMemcpyHostToDevice));
-  for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ctx->ev[k]));
+  for (int k = 0; k < 6; ++k) CK(cudaEventCreate(&ctx->ev[k]));
   // patch setup: 25 groups x levels, one CTA each
   int* d_status;
   CK(cudaMalloc(&d_status, sizeof(int)));
@@ -829,6 +849,7 @@ int svk_config_default(svk_config* cfg, int32_t n_elem) {
   cfg->nranks = 1;
   cfg->transport = SVK_TRANSPORT_NONE;
   cfg->agglom_rows = 64;
+  cfg->orth = SVK_ORTH_ADAPTIVE;
   return SVK_OK;
 }
 
@@ -846,6 +867,7 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
   }
   if (n != cfg->n_coarse) return SVK_ERR_INVALID;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return SVK_ERR_INVALID;
+  if (cfg->orth != SVK_ORTH_ADAPTIVE && cfg->orth != SVK_ORTH_CGS2) return SVK_ERR_INVALID;
   if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
                           (cfg->transport != SVK_TRANSPORT_NCCL && cfg->transport != SVK_TRANSPORT_EMULATED)))
     return SVK_ERR_INVALID;

@@ -21,6 +21,7 @@ PROBLEMS = {"zero": 0, "mms_paper": 1, "mms_inspace": 2, "cavity": 3}
 WEIGHTING = {"mult": 0, "scalar": 1}
 COARSE = {"exact": 0, "sweeps3": 1}
 SWEEP = {"fused": 0, "unfused": 1}
+ORTH = {"adaptive": 0, "cgs2": 1}
 TRANSPORT = {"none": 0, "nccl": 1, "emulated": 2}
 
 
@@ -33,7 +34,7 @@ class Config(C.Structure):
                 ("weighting", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("coarse", C.c_int32),
                 ("sweep_impl", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("transport", C.c_int32), ("agglom_rows", C.c_int32), ("emul_group", C.c_int32),
-                ("reserved", C.c_int32 * 3), ("nccl_id", C.c_uint8 * 128)]
+                ("orth", C.c_int32), ("reserved", C.c_int32 * 2), ("nccl_id", C.c_uint8 * 128)]
 
 
 class LevelInfo(C.Structure):
@@ -44,7 +45,7 @@ class LevelInfo(C.Structure):
 
 
 class Report(C.Structure):
-    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("n_reorth", C.c_int32),
                 ("rel_residual", C.c_double), ("t_total_s", C.c_double), ("t_vcycle_s", C.c_double),
                 ("t_orth_s", C.c_double)]
 
@@ -144,7 +145,8 @@ class Solver:
     def __init__(self, n_elem: int, n_coarse: int = 4, nu: float = 1.0, omega: float = 0.8,
                  weighting: str = "mult", nu_pre: int = 1, nu_post: int = 1, coarse: str = "exact",
                  sweep: str = "fused", device: int = 0, rank: int = 0, nranks: int = 1,
-                 transport: str = "none", agglom_rows: int = 64, emul_group: int = 0, nccl_id: bytes | None = None):
+                 transport: str = "none", agglom_rows: int = 64, emul_group: int = 0, nccl_id: bytes | None = None,
+                 orth: str = "adaptive"):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
         "emulated" runs nranks logical ranks of one process on one device (one thread each)."""
@@ -159,7 +161,7 @@ class Solver:
         cfg.weighting, cfg.nu_pre, cfg.nu_post = WEIGHTING[weighting], nu_pre, nu_post
         cfg.coarse, cfg.sweep_impl, cfg.device = COARSE[coarse], SWEEP[sweep], device
         cfg.rank, cfg.nranks, cfg.transport = rank, nranks, TRANSPORT[transport]
-        cfg.agglom_rows, cfg.emul_group = agglom_rows, emul_group
+        cfg.agglom_rows, cfg.emul_group, cfg.orth = agglom_rows, emul_group, ORTH[orth]
         if nccl_id is not None:
             if len(nccl_id) != 128:
                 raise SvkError("nccl_id must be 128 bytes")

@@ -184,6 +184,33 @@ def test_fgmres_iterations_and_solution(gpu, impl, N, kind):
     assert np.all(np.abs(hist[:k][m] - ho[:k][m]) <= 1e-6 * ho[:k][m])
 
 
+@pytest.mark.parametrize("N,kind", [(64, "mms_paper"), (256, "cavity")])
+def test_fgmres_orth_modes(gpu, N, kind):
+    """ADAPTIVE (one Gram-Schmidt pass unless it cancels; reading 18) and CGS2
+    reach the oracle's (MGS) iteration count and solution."""
+    O = get_oracle(N)
+    kcode = {"mms_paper": oracle.MMS_PAPER, "cavity": oracle.CAVITY}[kind]
+    bo, x0o = O.problem(kcode)
+    xo, its, ho, _, _ = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)
+    hists = {}
+    for orth in ("adaptive", "cgs2"):
+        S = get_solver(N, orth=orth)
+        b, x = S.set_problem(kind)
+        rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=100)
+        assert rep["converged"] == 1 and abs(rep["iterations"] - its) <= 1
+        if orth == "cgs2":
+            assert rep["n_reorth"] == rep["iterations"]
+        else:
+            assert 0 <= rep["n_reorth"] <= rep["iterations"]
+        xg = to_np(S, x, S.fine)
+        nv = (2 * N + 1) ** 2
+        assert np.abs(xg[:2 * nv] - xo[:2 * nv]).max() < 1e-8 * max(np.abs(xo[:2 * nv]).max(), 1.0)
+        k = min(len(hist), len(ho))
+        m = ho[:k] > 1e-6
+        assert np.all(np.abs(hist[:k][m] - ho[:k][m]) <= 1e-6 * ho[:k][m])
+        hists[orth] = hist
+
+
 @pytest.mark.parametrize("N", [64, 512])
 def test_mms_nodal_exactness_gpu(gpu, N):
     """Closed-form pin at any size: the converged solution equals the paper's
