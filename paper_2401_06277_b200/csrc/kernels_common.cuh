@@ -190,15 +190,6 @@ __global__ void k_set_problem(LevelGeom g, int kind, double nu, double* __restri
 //   f = 4e+3 : 2e, 2e+1, 2e+2  (-1/8, 3/4, 3/8)
 // 1D Q1: fine 2e -> coarse e (1); fine 2e+1 -> e, e+1 (1/2, 1/2)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int p2row(int f, int* c, double* w) {
-  const int m = f & 3, e = f >> 2;
-  if (m == 0) { c[0] = 2 * e; w[0] = 1.0; return 1; }
-  if (m == 2) { c[0] = 2 * e + 1; w[0] = 1.0; return 1; }
-  c[0] = 2 * e; c[1] = 2 * e + 1; c[2] = 2 * e + 2;
-  if (m == 1) { w[0] = 0.375; w[1] = 0.75; w[2] = -0.125; }
-  else { w[0] = -0.125; w[1] = 0.75; w[2] = 0.375; }
-  return 3;
-}
 // P^T column (coarse lattice c): fine indices 2c + off
 __device__ __forceinline__ int p2col(int c, int* f, double* w) {
   if (c & 1) {
@@ -211,38 +202,72 @@ __device__ __forceinline__ int p2col(int c, int* f, double* w) {
   return 5;
 }
 
-// x_f += P e_c on non-Dirichlet fine points (Dirichlet rows of P e_c are 0),
-// owned rows of the slab only (lattice rows [2 r0, 2 r1), node rows [r0, r1))
-__global__ void k_prolong_add(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec, double* __restrict__ xf) {
-  const int plane = blockIdx.z;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y + (plane < 2 ? 2 * gf.r0 : gf.r0);
-  if (plane < 2) {
-    if (j >= 2 * gf.r1) return;
-    if (i < 1 || j < 1 || i >= gf.lat - 1 || j >= gf.lat - 1) return;
-    int cx[3], cy[3];
-    double wx[3], wy[3];
-    const int nx = p2row(i, cx, wx), ny = p2row(j, cy, wy);
-    const double* e = ec + (plane ? gc.ouy : gc.oux);
-    double s = 0.0;
-    for (int b = 0; b < ny; ++b) {
-      double t = 0.0;
-      for (int a = 0; a < nx; ++a) t += wx[a] * e[(int64_t)cy[b] * gc.pu + cx[a]];
-      s += wy[b] * t;
+// Vectorised prolongation x_f += P e_c (alg:mg "Correction"), the form
+// used by the V-cycle.  Velocity (1D Q2, fine lattice 4e+m from coarse lattice
+// 2e..2e+2: m=0 -> (1,0,0), 1 -> (3/8,3/4,-1/8), 2 -> (0,1,0), 3 -> (-1/8,3/4,3/8)):
+// one thread per coarse element (ex, ey) and component produces the 4x4 fine
+// points (4ex.., 4ey..) from its 3x3 coarse values -- 9 loads, 16 read-modify-
+// writes as double2.  Only the owned fine rows [2 r0, 2 r1) are written;
+// Dirichlet points (i or j = 0; 4 Nc is never produced) are left untouched.
+__global__ void __launch_bounds__(128) k_prolong_q2(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
+                                                    double* __restrict__ xf, int ey0) {
+  const int ex = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ey = ey0 + blockIdx.y * blockDim.y + threadIdx.y;
+  const int comp = blockIdx.z;
+  if (ex >= gc.N || ey >= gc.N) return;
+  const int jlo = max(2 * gf.r0, 1), jhi = min(2 * gf.r1, gf.lat - 1);
+  const double* e = ec + (comp ? gc.ouy : gc.oux) + (int64_t)(2 * ey) * gc.pu + 2 * ex;
+  double tx[3][4];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const double c0 = e[(int64_t)r * gc.pu], c1 = e[(int64_t)r * gc.pu + 1], c2 = e[(int64_t)r * gc.pu + 2];
+    tx[r][0] = ex == 0 ? 0.0 : c0;  // fine column 0 is Dirichlet
+    tx[r][1] = 0.375 * c0 + 0.75 * c1 - 0.125 * c2;
+    tx[r][2] = c1;
+    tx[r][3] = -0.125 * c0 + 0.75 * c1 + 0.375 * c2;
+  }
+  double* f = xf + (comp ? gf.ouy : gf.oux) + (int64_t)(4 * ey) * gf.pu + 4 * ex;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int j = 4 * ey + m;
+    if (j < jlo || j >= jhi) continue;
+    const double w0 = m == 0 ? 1.0 : m == 1 ? 0.375 : m == 2 ? 0.0 : -0.125;
+    const double w1 = m == 0 ? 0.0 : m == 1 ? 0.75 : m == 2 ? 1.0 : 0.75;
+    const double w2 = m == 0 ? 0.0 : m == 1 ? -0.125 : m == 2 ? 0.0 : 0.375;
+    double2* row = reinterpret_cast<double2*>(f + (int64_t)m * gf.pu);
+    double2 a = row[0], b = row[1];
+    a.x += w0 * tx[0][0] + w1 * tx[1][0] + w2 * tx[2][0];
+    a.y += w0 * tx[0][1] + w1 * tx[1][1] + w2 * tx[2][1];
+    b.x += w0 * tx[0][2] + w1 * tx[1][2] + w2 * tx[2][2];
+    b.y += w0 * tx[0][3] + w1 * tx[1][3] + w2 * tx[2][3];
+    row[0] = a;
+    row[1] = b;
+  }
+}
+// pressure (1D Q1: fine node 2a <- a, 2a+1 <- (a, a+1)/2): one thread per coarse
+// node (ax, ay) produces fine nodes (2ax, 2ax+1) x (2ay, 2ay+1); owned rows only.
+__global__ void __launch_bounds__(128) k_prolong_q1(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
+                                                    double* __restrict__ xf, int ay0) {
+  const int ax = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ay = ay0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (ax > gc.N || ay > gc.N) return;
+  const double* e = ec + gc.op + (int64_t)ay * gc.pp + ax;
+  const bool rx = ax < gc.N, ry = ay < gc.N;  // neighbours exist
+  const double c00 = e[0], c10 = rx ? e[1] : 0.0, c01 = ry ? e[gc.pp] : 0.0, c11 = rx && ry ? e[gc.pp + 1] : 0.0;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {
+    const int j = 2 * ay + dy;
+    if (j < gf.r0 || j >= gf.r1 || j > gf.N) continue;
+    const double l = dy ? 0.5 * (c00 + c01) : c00, r = dy ? 0.5 * (c10 + c11) : c10;
+    double* f = xf + gf.op + (int64_t)j * gf.pp + 2 * ax;
+    if (rx) {
+      double2 v = *reinterpret_cast<double2*>(f);
+      v.x += l;
+      v.y += 0.5 * (l + r);
+      *reinterpret_cast<double2*>(f) = v;
+    } else {
+      f[0] += l;
     }
-    xf[(plane ? gf.ouy : gf.oux) + (int64_t)j * gf.pu + i] += s;
-  } else {
-    if (i > gf.N || j > gf.N || j >= gf.r1) return;
-    const int ax = i >> 1, ay = j >> 1;
-    const double* e = ec + gc.op;
-    double s;
-    if (!(i & 1) && !(j & 1)) s = e[(int64_t)ay * gc.pp + ax];
-    else if (!(j & 1)) s = 0.5 * (e[(int64_t)ay * gc.pp + ax] + e[(int64_t)ay * gc.pp + ax + 1]);
-    else if (!(i & 1)) s = 0.5 * (e[(int64_t)ay * gc.pp + ax] + e[(int64_t)(ay + 1) * gc.pp + ax]);
-    else
-      s = 0.25 * (e[(int64_t)ay * gc.pp + ax] + e[(int64_t)ay * gc.pp + ax + 1] + e[(int64_t)(ay + 1) * gc.pp + ax] +
-                  e[(int64_t)(ay + 1) * gc.pp + ax + 1]);
-    xf[p_at(gf, i, j)] += s;
   }
 }
 

@@ -42,6 +42,8 @@ struct svk_ctx {
   std::vector<double*> ws_x, ws_t, ws_r, ws_b;
   double* d_dbuf = nullptr;  // packed patch buffer (unfused sweep), finest-level size
   double* d_bd = nullptr;    // boundary-patch corrections (fused sweep), finest-level size
+  std::vector<BdTile*> d_tiles;  // per level: boundary-patch tiles (k_boundary_patches)
+  std::vector<int> ntiles;
   double* d_sw = nullptr;    // extra ping-pong vector for nsweeps > 1, finest-level size
   // Krylov
   std::vector<double*> V, Z;
@@ -371,8 +373,8 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
     TRY(launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
-                           ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_bd, x_zero ? nullptr : xin, b, xout,
-                           ctx->nsm, s));
+                           ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_tiles[l], ctx->ntiles[l], ctx->d_bd,
+                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s));
     CKL();
     ctx->launches++;  // two kernels: boundary patches + fused sweep
     return SVK_OK;
@@ -398,7 +400,18 @@ int op_restrict(svk_ctx* ctx, int l, const double* rf, double* rc, cudaStream_t 
   return SVK_OK;
 }
 int op_prolong_add(svk_ctx* ctx, int l, const double* ec, double* xf, cudaStream_t s) {
-  k_prolong_add<<<plane_grid(ctx->g[l]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], ec, xf);
+  const LevelGeom &gf = ctx->g[l], &gc = ctx->g[l - 1];
+  // velocity: coarse element rows covering the owned fine lattice rows [max(2 r0, 1), min(2 r1, lat - 1))
+  const int jlo = std::max(2 * gf.r0, 1), jhi = std::min(2 * gf.r1, gf.lat - 1);
+  if (jhi > jlo) {
+    const int ey0 = jlo / 4, ney = (jhi - 1) / 4 - ey0 + 1;
+    const dim3 blk(32, 4), grd((unsigned)((gc.N + 31) / 32), (unsigned)((ney + 3) / 4), 2);
+    k_prolong_q2<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ey0);
+    CKL();
+  }
+  const int ay0 = gf.r0 / 2, nay = (gf.r1 - 1) / 2 - ay0 + 1;
+  const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((nay + 3) / 4), 1);
+  k_prolong_q1<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ay0);
   CKL();
   return SVK_OK;
 }
@@ -699,6 +712,7 @@ int free_ctx(svk_ctx* ctx) {
     for (double* p : *v) F(p);
   F(ctx->d_dbuf);
   F(ctx->d_bd);
+  for (BdTile* p : ctx->d_tiles) F(p);
   F(ctx->d_sw);
   for (double* p : ctx->V) F(p);
   for (double* p : ctx->Z) F(p);
@@ -816,6 +830,14 @@ int create_impl(svk_ctx* ctx) {
     TRY(alloc_vec(ctx, &ctx->ws_r[l], n));
   }
   TRY(alloc_vec(ctx, &ctx->d_bd, (int64_t)kSlots * bd_count(ctx->g.back().N)));
+  for (int l = 0; l < ctx->nlev; ++l) {
+    const std::vector<BdTile> t = make_bd_tiles(ctx->g[l].N);
+    BdTile* d = nullptr;
+    CK(cudaMalloc(&d, t.size() * sizeof(BdTile)));
+    ctx->d_tiles.push_back(d);
+    ctx->ntiles.push_back((int)t.size());
+    CK(cudaMemcpy(d, t.data(), t.size() * sizeof(BdTile), cudaMemcpyHostToDevice));
+  }
   if (c.sweep_impl == SVK_SWEEP_UNFUSED) {
     const LevelGeom& gf = ctx->g.back();
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));

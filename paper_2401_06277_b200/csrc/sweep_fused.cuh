@@ -16,7 +16,10 @@
 // (169 FMA instead of 625), and bx lives only in EO, by only in OE.
 #pragma once
 #include <cuda.h>
+#include <algorithm>
 #include <cstring>
+#include <vector>
+
 #include "stencil.cuh"
 
 namespace svk {
@@ -182,48 +185,78 @@ __host__ __device__ __forceinline__ int64_t bd_index(int kx, int ky, int N) {
   return 4 * (int64_t)(N + 1) + (int64_t)bd_axis(kx, N) * (N - 3) + (ky - 2);
 }
 
-__global__ void __launch_bounds__(64) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
-                                                        const double* __restrict__ x, const double* __restrict__ b,
-                                                        double* __restrict__ bd) {
+// Tiles of boundary patches that share one group (category pair): patches
+// (kx + q dx, ky + q dy), q < n.  One CTA per tile stages the group's padded
+// inverse in shared memory once (instead of once per patch), evaluates the
+// tile's window residuals, then applies the inverse (same summation order as a
+// per-patch dense product).
+struct BdTile {
+  int kx, ky, dx, dy, n, grp;
+};
+constexpr int kBdTile = 16, kBdThreads = 512;
+inline std::vector<BdTile> make_bd_tiles(int N) {
+  std::vector<BdTile> t;
+  auto seg = [&](int kx, int ky, int dx, int dy, int n) {
+    for (int q0 = 0; q0 < n; q0 += kBdTile)
+      t.push_back(BdTile{kx + q0 * dx, ky + q0 * dy, dx, dy, std::min(kBdTile, n - q0), pcat(ky, N) * 5 + pcat(kx, N)});
+  };
+  const int rows[4] = {0, 1, N - 1, N};
+  for (int ky : rows) {
+    seg(0, ky, 1, 0, 1);
+    seg(1, ky, 1, 0, 1);
+    seg(2, ky, 1, 0, N - 3);
+    seg(N - 1, ky, 1, 0, 1);
+    seg(N, ky, 1, 0, 1);
+  }
+  for (int kx : rows) seg(kx, 2, 0, 1, N - 3);
+  return t;
+}
+
+__global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
+                                                         const BdTile* __restrict__ tiles,
+                                                         const double* __restrict__ x, const double* __restrict__ b,
+                                                         double* __restrict__ bd) {
+  constexpr int T = kBdTile, RS = 53;  // odd row stride: conflict-free 64-bit smem accesses
+  __shared__ double Ai[kGroupStride];
+  __shared__ double rv[T * RS];
   const int N = g.N, lat = g.lat;
   const int64_t nb = bd_count(N);
-  const int64_t id = blockIdx.x;
-  int kx, ky;
-  if (id < 4 * (int64_t)(N + 1)) {
-    const int r = (int)(id / (N + 1));
-    ky = r <= 1 ? r : r + N - 3;
-    kx = (int)(id % (N + 1));
-  } else {
-    const int64_t q = id - 4 * (int64_t)(N + 1);
-    const int c = (int)(q / (N - 3));
-    kx = c <= 1 ? c : c + N - 3;
-    ky = 2 + (int)(q % (N - 3));
-  }
-  if (ky < g.r0 - 1 || ky > g.r1) return;  // patch rows a slab's sweep uses: r0-1 .. r1
-  __shared__ double rv[kSlots];
-  const int s = threadIdx.x;
-  if (s < kSlots) {
+  const BdTile tl = tiles[blockIdx.x];
+  const int ylo = tl.ky + (tl.n - 1) * tl.dy;
+  if (max(tl.ky, ylo) < g.r0 - 1 || min(tl.ky, ylo) > g.r1) return;  // patch rows a slab uses: r0-1 .. r1
+  const double* A = dinv + (size_t)tl.grp * kGroupStride;
+  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) Ai[q] = A[q];
+  for (int q = threadIdx.x; q < T * kSlots; q += blockDim.x) {
+    const int pi = q % T, s = q / T;  // consecutive threads -> consecutive patches
     double r = 0.0;
-    if (s < 50) {
-      const int comp = s / 25, oy = (s % 25) / 5, ox = s % 5;
-      const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
-      if (i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
-        const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-        double ax = 0.0;
-        if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
-        r = b[o] - ax;
+    if (pi < tl.n) {
+      const int kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
+      if (s < 50) {
+        const int comp = s / 25, oy = (s % 25) / 5, ox = s % 5;
+        const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+        if (i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
+          const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
+          double ax = 0.0;
+          if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
+          r = b[o] - ax;
+        }
+      } else {
+        const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
+        r = b[p_at(g, kx, ky)] - ax;
       }
-    } else {
-      const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
-      r = b[p_at(g, kx, ky)] - ax;
     }
-    rv[s] = r;
+    rv[pi * RS + s] = r;
   }
   __syncthreads();
-  if (s < kSlots) {
-    const double* A = dinv + (size_t)(pcat(ky, N) * 5 + pcat(kx, N)) * kGroupStride + s * kSlots;
+  for (int q = threadIdx.x; q < T * kSlots; q += blockDim.x) {
+    const int pi = q % T, s = q / T;
+    if (pi >= tl.n) continue;
+    const int kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
+    if (ky < g.r0 - 1 || ky > g.r1) continue;
+    const double* Ar = Ai + s * kSlots;
+    const double* rr = rv + pi * RS;
     double d = 0.0;
-    for (int q = 0; q < kSlots; ++q) d = fma(A[q], rv[q], d);
+    for (int c = 0; c < kSlots; ++c) d = fma(Ar[c], rr[c], d);
     bd[(int64_t)s * nb + bd_index(kx, ky, N)] = d;
   }
 }
@@ -808,9 +841,9 @@ inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsi
 }
 
 inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,
-                              const double* dinv, double* bd, const double* xin, const double* b, double* xout,
-                              int nsm, cudaStream_t s) {
-  k_boundary_patches<<<(unsigned)bd_count(g.N), 64, 0, s>>>(g, nu, dinv, xin, b, bd);
+                              const double* dinv, const BdTile* tiles, int ntiles, double* bd, const double* xin,
+                              const double* b, double* xout, int nsm, cudaStream_t s) {
+  k_boundary_patches<<<(unsigned)ntiles, kBdThreads, 0, s>>>(g, nu, dinv, tiles, xin, b, bd);
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
