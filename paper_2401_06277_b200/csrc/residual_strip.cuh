@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
     spE = 2 * Y1;
   }
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + rz::OMB);
-  unsigned phase[2] = {0u, 0u};
+  unsigned phases = 0u;  // bit b: parity of mbarrier b
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   auto rprow4 = [&](int r) { return rz::ORP + (r & 3) * fz::PWID; };
   for (int sp = spB; sp <= spE; ++sp) {
     const int k = sp - spB;
-    mbar_wait(&bars[k & 1], phase[k & 1]);
-    phase[k & 1] ^= 1u;
+    mbar_wait(&bars[k & 1], (phases >> (k & 1)) & 1u);
+    phases ^= 1u << (k & 1);
     if (t == 0) {  // prefetch step sp+1: x pair sp+2, p row sp+3, b pair sp+1, b_p row sp+2
       uint64_t* nb = &bars[(k + 1) & 1];
       mbar_expect_tx(nb, fz::kXBytes + fz::kPBytes + (NOB ? 0u : fz::kBBytes + fz::kBPBytes));
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
     }
     __syncthreads();
   }
-  mbar_wait(&bars[(spE - spB + 1) & 1], phase[(spE - spB + 1) & 1]);
+  mbar_wait(&bars[(spE - spB + 1) & 1], (phases >> ((spE - spB + 1) & 1)) & 1u);
 }
 
 // MODE 0: out = b - A x (NOB = false) or A x (NOB = true) on level g.

@@ -32,6 +32,11 @@ struct StencilConst {
   // 1D columns of C^, G at non-Dirichlet lattice points: even i = 2a touches
   // nodes a-1, a, a+1 ([0][0..2]); odd i = 2a+1 touches nodes a, a+1 ([1][0..1])
   double CC[2][3], GC[2][3];
+  // the (unscaled) B rows at a pressure node of class (cy, cx) in {0,1,2}^2 over its 5x5
+  // window, per component: PB[0] = C^R[cy] (x) GR[cx], PB[1] = GR[cy] (x) C^R[cx]
+  // (B_x = -h PB[0], B_y = -h PB[1]); a table indexed by the node class so that the
+  // boundary-node branch of the fused kernels holds no loop-invariant registers
+  double PB[2][9][25];
 };
 
 // pitched vector layout of one level (see include/svk.h)

@@ -158,6 +158,13 @@ bool build_tables(StencilConst& t, std::string& err) {
       t.GR[cls][o] = at(g1, k, 2 * k - 2 + o, lat);
     }
   }
+  for (int cy = 0; cy < 3; ++cy)
+    for (int cx = 0; cx < 3; ++cx)
+      for (int r = 0; r < 5; ++r)
+        for (int o = 0; o < 5; ++o) {
+          t.PB[0][cy * 3 + cx][r * 5 + o] = t.CR[cy][r] * t.GR[cx][o];
+          t.PB[1][cy * 3 + cx][r * 5 + o] = t.GR[cy][r] * t.CR[cx][o];
+        }
   // columns at non-Dirichlet lattice points (checked uniform)
   for (int i = 1; i < lat - 1; ++i) {
     const int par = i & 1;

@@ -464,14 +464,15 @@ __device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, c
         bu = fma(F.PBY[r][2], V[r][2], bu);
         bu = fma(F.PBY[r][3], V[r][3], bu);
       }
-    } else if (pok) {  // boundary pressure node: general rows from the class tables
-      const int cx = na == 0 ? 0 : (na == N ? 2 : 1), cy = nrow == 0 ? 0 : (nrow == N ? 2 : 1);
+    } else if (pok) {  // boundary pressure node: its B rows from the class table (B = -h PB)
+      const int cls = (nrow == 0 ? 0 : (nrow == N ? 2 : 1)) * 3 + (na == 0 ? 0 : (na == N ? 2 : 1));
+      const double* pbx = c_st.PB[0][cls];
+      const double* pby = c_st.PB[1][cls];
       double sacc = 0.0;
 #pragma unroll
       for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int ox = 0; ox < 5; ++ox)
-          sacc += c_st.CR[cy][r] * c_st.GR[cx][ox] * U[r][ox] + c_st.GR[cy][r] * c_st.CR[cx][ox] * V[r][ox];
+        for (int ox = 0; ox < 5; ++ox) sacc = fma(pby[r * 5 + ox], V[r][ox], fma(pbx[r * 5 + ox], U[r][ox], sacc));
       bu = -g.h * sacc;
     }
     ax[0] += F.GX[1][0][0][0] * Pm[0][0] + F.GX[1][0][0][2] * Pm[0][2] + F.GX[1][0][1][0] * Pm[1][0] +
@@ -591,25 +592,6 @@ __device__ __forceinline__ double solve_generic(double (&vx)[25], double (&vy)[2
   return dp;
 }
 
-// issue the TMA loads a step needs (one elected thread): x row pair p (rows 2p+1,
-// 2p+2) both components, p row pr, b row pair pb, b_p row rbp
-template <bool XZERO>
-__device__ __forceinline__ void issue_loads(double* sm, const FusedMaps& M, uint64_t* bar, int xc0, int pc0, int kx0,
-                                            int xp, int pr, int pb, int rbp, bool with_x, bool with_b) {
-  unsigned bytes = 0;
-  if (!XZERO && with_x) bytes += fz::kXBytes + fz::kPBytes;
-  if (with_b) bytes += fz::kBBytes + fz::kBPBytes;
-  mbar_expect_tx(bar, bytes);
-  if (!XZERO && with_x) {
-    tma_load_3d(sm + xpair(xp), &M.xv, xc0, 2 * xp + 1, 0, bar);
-    tma_load_2d(sm + prow(pr), &M.xp, pc0, pr, bar);
-  }
-  if (with_b) {
-    tma_load_3d(sm + bpair(pb), &M.bv, xc0 + 2, 2 * pb + 1, 0, bar);
-    tma_load_2d(sm + bprow(rbp), &M.bp, kx0 - 2, rbp, bar);
-  }
-}
-
 template <bool XZERO>
 __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F,
                                                             const __grid_constant__ FusedMaps M) {
@@ -624,7 +606,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   const int xc0 = 2 * kx0 - 6, pc0 = kx0 - 4;
   const int sB = y0 - 1, sE = y1;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + fz::OMB);
-  unsigned phase[2] = {0u, 0u};
+  unsigned phases = 0u;  // bit b: parity of mbarrier b (a register, not a local array)
 
   if (t == 0) {
     mbar_init(&bars[0], 1);
@@ -644,8 +626,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     for (int p = sB - 2; p <= sB - 1; ++p) tma_load_3d(sm + bpair(p), &M.bv, xc0 + 2, 2 * p + 1, 0, &bars[0]);
     for (int r = sB - 1; r <= sB; ++r) tma_load_2d(sm + bprow(r), &M.bp, kx0 - 2, r, &bars[0]);
   }
-  mbar_wait(&bars[0], phase[0]);
-  phase[0] ^= 1u;
+  mbar_wait(&bars[0], 0u);
+  phases ^= 1u;
   fused_residual<XZERO>(sm, A.g, F, sB - 2, kx0);
   fused_residual<XZERO>(sm, A.g, F, sB - 1, kx0);
   __syncthreads();
@@ -683,8 +665,9 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     //   b_p row s+2 -> slot of row s (step s-1 residual)
     //   residual rows 2s+1, 2s+2 -> slots of rows 2s-6, 2s-5 (step s-2's solve)
     //   pressure residual row s+1 -> slot of row s-3 (step s-3's solve)
-    mbar_wait(&bars[(s - sB + 1) & 1], phase[(s - sB + 1) & 1]);
-    phase[(s - sB + 1) & 1] ^= 1u;
+    const int bi = (s - sB + 1) & 1;
+    mbar_wait(&bars[bi], (phases >> bi) & 1u);
+    phases ^= 1u << bi;
     uint64_t* nbar = &bars[(s - sB) & 1];
     if (t == 0) {
       unsigned bytes = fz::kBBytes + fz::kBPBytes + (XZERO ? 0u : fz::kXBytes + fz::kPBytes);
@@ -778,7 +761,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     }
   }
   // the last prefetch (for step sE+1) must land before the CTA's shared memory is released
-  mbar_wait(&bars[(sE - sB) & 1], phase[(sE - sB) & 1]);
+  mbar_wait(&bars[(sE - sB) & 1], (phases >> ((sE - sB) & 1)) & 1u);
 }
 
 inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const double* /*d_inv*/, double* d_fac,

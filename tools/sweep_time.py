@@ -1,0 +1,17 @@
+"""Device time of one fused sweep (x random) and one V-cycle at N (development aid)."""
+import sys
+
+import torch
+
+from paper_2401_06277_b200 import Solver
+from tools.perf_probe import ev_time
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+S = Solver(N)
+b, x = S.set_problem("mms_paper")
+x = torch.randn_like(b)
+out = S.new_vector()
+t = ev_time(lambda: S.sweep(S.fine, x, b, out=out), reps=20)
+nodes = (N + 1) ** 2
+tv = ev_time(lambda: S.vcycle(b, out), reps=10)
+print(f"N={N} sweep {t*1e3:.3f} ms ({216*nodes/t/1e9:.0f} GB/s alg, {1316*nodes/t/1e12:.2f} TF alg)  vcycle {tv*1e3:.3f} ms", flush=True)
