@@ -27,6 +27,7 @@ _lock = threading.Lock()
 _lib = None
 
 MMS_ZERO, MMS_PAPER, MMS_INSPACE, CAVITY = 0, 1, 2, 3
+RELAX_VANKA, RELAX_BS, RELAX_SU = 0, 1, 2
 WEIGHT_MULT, WEIGHT_SCALAR = 0, 1
 
 
@@ -77,6 +78,10 @@ def _load():
             "orc_fgmres": (I, [P, P, P, D, I, P, P, P]),
             "orc_sweep_sample": (None, [I, D, D, I, P, P, P, I64, P]),
             "orc_residual_sample": (None, [I, D, P, P, P, I64, P]),
+            "orc_set_relax": (I, [P, I, D, D, D, I]),
+            "orc_relax_sweep": (None, [P, I, P, P, P]),
+            "orc_schur_nnz": (I64, [P, I]),
+            "orc_schur_csr": (None, [P, I, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -234,6 +239,32 @@ class Oracle:
             self._lib.orc_vanka_sweep(self._h, level, _ptr(x), _ptr(b), _ptr(out))
             x, out = out, x
         return x
+
+    def set_relax(self, kind: int, t: float = 1.0, omega_r: float = 1.0, omega_j: float = 0.8, nj: int = 3):
+        """V-cycle relaxation: RELAX_VANKA (alg:vk), RELAX_BS (inexact Braess-Sarazin,
+        alg:bs; omega_r = omega_BS) or RELAX_SU (Schur-Uzawa, alg:uz; omega_r unused);
+        t scales D = diag(L); omega_j, nj: weighted Jacobi on S = -(1/t) B D^-1 B^T."""
+        if self._lib.orc_set_relax(self._h, kind, t, omega_r, omega_j, nj) != 0:
+            raise ValueError("oracle: bad relaxation parameters")
+        self.relax_kind = kind
+
+    def relax_sweep(self, level: int, x, b) -> np.ndarray:
+        """One sweep of the configured relaxation (Vanka by default)."""
+        x, b = _f64(x), _f64(b)
+        out = np.zeros_like(x)
+        self._lib.orc_relax_sweep(self._h, level, _ptr(x), _ptr(b), _ptr(out))
+        return out
+
+    def schur(self, level: int):
+        """S = -(1/t) B D^{-1} B^T on level `level` (after set_relax with BS or SU)."""
+        import scipy.sparse as sp
+        n = (self.N(level) + 1) ** 2
+        nnz = int(self._lib.orc_schur_nnz(self._h, level))
+        rp = np.zeros(n + 1, np.int64)
+        col = np.zeros(nnz, np.int32)
+        val = np.zeros(nnz, np.float64)
+        self._lib.orc_schur_csr(self._h, level, _ptr(rp), _ptr(col), _ptr(val))
+        return sp.csr_matrix((val, col, rp), shape=(n, n))
 
     def restrict(self, level: int, rf) -> np.ndarray:
         rf = _f64(rf)

@@ -73,6 +73,13 @@ struct Level {
   std::vector<double> weight;  // diagonal of W_i, per global DOF (see reading 6)
   // interpolation from level-1 (coarse) into this level
   Csr P, PT;
+  // Braess-Sarazin / Schur-Uzawa comparators (alg:bs P:236-241, alg:uz P:313-320):
+  // Dinv = 1/diag(L) on non-Dirichlet velocity DOFs (0 elsewhere), indexed by
+  // global DOF (< 2 nv); S = -(1/t) B D^{-1} B^T as an explicit pressure x pressure
+  // CSR (indices relative to the pressure block) and its diagonal.
+  std::vector<double> Dinv;
+  Csr S;
+  std::vector<double> Sdiag;
   // level-0 direct solve (reading 3: minimum-norm)
   std::vector<int64_t> interior;
   std::vector<double> clu;
@@ -85,6 +92,12 @@ struct Ctx {
   int weighting = 0;  // 0: W_i = omega*diag(1/mult); 1: W_i = omega*I
   int nu1 = 1, nu2 = 1;
   int coarse_mode = 0;  // 0: exact min-norm solve; 1: three Vanka sweeps
+  // relaxation inside the V-cycle: 0 Vanka (alg:vk), 1 inexact Braess-Sarazin
+  // (alg:bs), 2 Schur-Uzawa (alg:uz); t scales D, omega_r = omega_BS (BS only),
+  // omega_j / nj = weight / sweeps of the Jacobi iteration on S
+  int relax = 0;
+  double t = 1.0, omega_r = 1.0, omega_j = 0.8;
+  int nj = 3;
   std::vector<Level> lev;
   std::string err;
 };
@@ -438,6 +451,127 @@ void vanka_sweep(const Level& L, const double* xin, const double* b, double* xou
 }
 
 // --------------------------------------------------------------------------
+// Braess-Sarazin and Schur-Uzawa, the paper's same-run
+// comparators.  Everything is taken from the assembled CSR A:
+//   B   = pressure rows of A restricted to velocity columns (eq:stokesmatrix),
+//   B^T = velocity rows of A restricted to pressure columns (A is symmetric; the
+//         Dirichlet velocity rows are identity rows, so they hold no B^T entries),
+//   D   = diag(L) on the non-Dirichlet velocity DOFs (Dirichlet: D^{-1} := 0, the
+//         correction there stays 0),
+//   S   = -(1/t) B D^{-1} B^T, formed entry by entry as an explicit
+//         sparse product  S_km = -(1/t) sum_j B_kj D^{-1}_j B_mj.
+// --------------------------------------------------------------------------
+void build_schur(Level& L, double t) {
+  const int64_t nvel = 2 * L.nv, np = L.np;
+  L.Dinv.assign(nvel, 0.0);
+  for (int64_t r = 0; r < nvel; ++r) {
+    if (L.dir[r]) continue;
+    for (int64_t q = L.A.rowptr[r]; q < L.A.rowptr[r + 1]; ++q)
+      if (L.A.col[q] == r) L.Dinv[r] = 1.0 / L.A.val[q];
+  }
+  L.S = Csr();
+  L.S.nrows = np;
+  L.S.rowptr.assign(np + 1, 0);
+  L.Sdiag.assign(np, 0.0);
+  std::vector<std::map<int32_t, double>> rows(np);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t k = 0; k < np; ++k) {
+    const int64_t rk = nvel + k;
+    std::map<int32_t, double>& acc = rows[k];
+    for (int64_t q = L.A.rowptr[rk]; q < L.A.rowptr[rk + 1]; ++q) {
+      const int64_t j = L.A.col[q];
+      if (j >= nvel || L.Dinv[j] == 0.0) continue;
+      const double bkj = L.A.val[q] * L.Dinv[j];
+      for (int64_t q2 = L.A.rowptr[j]; q2 < L.A.rowptr[j + 1]; ++q2) {  // B^T_{j m} = A_{j, nvel+m}
+        const int64_t m = L.A.col[q2];
+        if (m < nvel) continue;
+        acc[(int32_t)(m - nvel)] += bkj * L.A.val[q2];
+      }
+    }
+  }
+  for (int64_t k = 0; k < np; ++k) {
+    for (auto& kv : rows[k]) {
+      L.S.col.push_back(kv.first);
+      L.S.val.push_back(-kv.second / t);
+      if (kv.first == k) L.Sdiag[k] = -kv.second / t;
+    }
+    L.S.rowptr[k + 1] = (int64_t)L.S.col.size();
+  }
+}
+
+// y_p = B v_u (v_u: the velocity part of a full vector)
+void apply_B(const Level& L, const double* v, double* y) {
+  const int64_t nvel = 2 * L.nv;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < L.np; ++k) {
+    double s = 0;
+    for (int64_t q = L.A.rowptr[nvel + k]; q < L.A.rowptr[nvel + k + 1]; ++q)
+      if (L.A.col[q] < nvel) s += L.A.val[q] * v[L.A.col[q]];
+    y[k] = s;
+  }
+}
+// y_u = B^T p (p: pressure block), 0 on Dirichlet velocity rows
+void apply_BT(const Level& L, const double* p, double* y) {
+  const int64_t nvel = 2 * L.nv;
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < nvel; ++j) {
+    double s = 0;
+    for (int64_t q = L.A.rowptr[j]; q < L.A.rowptr[j + 1]; ++q)
+      if (L.A.col[q] >= nvel) s += L.A.val[q] * p[L.A.col[q] - nvel];
+    y[j] = L.dir[j] ? 0.0 : s;
+  }
+}
+// nj sweeps of weighted Jacobi on S dp = rhs from dp = 0 ("standard weighted Jacobi")
+void schur_jacobi(const Level& L, const double* rhs, double omega_j, int nj, double* dp) {
+  std::vector<double> sdp(L.np);
+  for (int64_t k = 0; k < L.np; ++k) dp[k] = 0.0;
+  for (int it = 0; it < nj; ++it) {
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < L.np; ++k) {
+      double s = 0;
+      for (int64_t q = L.S.rowptr[k]; q < L.S.rowptr[k + 1]; ++q) s += L.S.val[q] * dp[L.S.col[q]];
+      sdp[k] = s;
+    }
+    for (int64_t k = 0; k < L.np; ++k) dp[k] += omega_j * (rhs[k] - sdp[k]) / L.Sdiag[k];
+  }
+}
+// alg:bs: inexact Braess-Sarazin, x_out = x_in + omega_BS (du, dp)
+//   S dp = r_p - (1/t) B D^{-1} r_u   (eq:bseq1, approximately by Jacobi)
+//   du   = (1/t) D^{-1} (r_u - B^T dp)  (eq:bseq2)
+void bs_sweep(const Ctx& c, const Level& L, const double* xin, const double* b, double* xout) {
+  const int64_t nvel = 2 * L.nv;
+  std::vector<double> r(L.ntot), w(nvel), rhs(L.np), dp(L.np), btdp(nvel);
+  residual(L, xin, b, r.data());
+  for (int64_t j = 0; j < nvel; ++j) w[j] = L.Dinv[j] * r[j] / c.t;
+  apply_B(L, w.data(), rhs.data());
+  for (int64_t k = 0; k < L.np; ++k) rhs[k] = r[nvel + k] - rhs[k];
+  schur_jacobi(L, rhs.data(), c.omega_j, c.nj, dp.data());
+  apply_BT(L, dp.data(), btdp.data());
+  for (int64_t j = 0; j < nvel; ++j) xout[j] = xin[j] + c.omega_r * (L.Dinv[j] * (r[j] - btdp[j]) / c.t);
+  for (int64_t k = 0; k < L.np; ++k) xout[nvel + k] = xin[nvel + k] + c.omega_r * dp[k];
+}
+// alg:uz: Schur-Uzawa, the block lower-triangular system eq:uzblock
+//   t D du = r_u ;  S dp = r_p - B du  (reading 19: alg:uz's
+//   "S dp = B du - r_p" contradicts eq:uzblock by a sign; eq:uzblock is followed)
+void su_sweep(const Ctx& c, const Level& L, const double* xin, const double* b, double* xout) {
+  const int64_t nvel = 2 * L.nv;
+  std::vector<double> r(L.ntot), du(nvel), rhs(L.np), dp(L.np);
+  residual(L, xin, b, r.data());
+  for (int64_t j = 0; j < nvel; ++j) du[j] = L.Dinv[j] * r[j] / c.t;
+  apply_B(L, du.data(), rhs.data());
+  for (int64_t k = 0; k < L.np; ++k) rhs[k] = r[nvel + k] - rhs[k];
+  schur_jacobi(L, rhs.data(), c.omega_j, c.nj, dp.data());
+  for (int64_t j = 0; j < nvel; ++j) xout[j] = xin[j] + du[j];
+  for (int64_t k = 0; k < L.np; ++k) xout[nvel + k] = xin[nvel + k] + dp[k];
+}
+// one relaxation sweep of the configured kind ("Relax on u_l and p_l", alg:mg)
+void relax(const Ctx& c, const Level& L, const double* xin, const double* b, double* xout) {
+  if (c.relax == 1) bs_sweep(c, L, xin, b, xout);
+  else if (c.relax == 2) su_sweep(c, L, xin, b, xout);
+  else vanka_sweep(L, xin, b, xout);
+}
+
+// --------------------------------------------------------------------------
 // Interpolation P_{l-1}: coarse -> fine, the finite-element interpolation of the
 // nested Q2 / Q1 spaces: row of a fine DOF = coarse basis functions
 // evaluated at the fine DOF's coordinates.
@@ -568,13 +702,13 @@ void mg(const Ctx& c, int l, const double* b, double* x) {
     if (c.coarse_mode == 0) coarse_solve(L, b, x);
     else {
       std::vector<double> t(L.ntot);
-      for (int s = 0; s < 3; ++s) { vanka_sweep(L, x, b, t.data()); std::copy(t.begin(), t.end(), x); }
+      for (int s = 0; s < 3; ++s) { relax(c, L, x, b, t.data()); std::copy(t.begin(), t.end(), x); }
     }
     return;
   }
   std::vector<double> t(L.ntot), r(L.ntot);
   for (int s = 0; s < c.nu1; ++s) {  // "Relax on u_l and p_l"
-    vanka_sweep(L, x, b, t.data());
+    relax(c, L, x, b, t.data());
     std::copy(t.begin(), t.end(), x);
   }
   residual(L, x, b, r.data());  // "Compute residual"
@@ -585,14 +719,14 @@ void mg(const Ctx& c, int l, const double* b, double* x) {
     if (c.coarse_mode == 0) coarse_solve(C, rc.data(), ec.data());  // "e_0 = A_0^{-1} r_0"
     else {
       std::vector<double> t0(C.ntot);
-      for (int s = 0; s < 3; ++s) { vanka_sweep(C, ec.data(), rc.data(), t0.data()); ec = t0; }
+      for (int s = 0; s < 3; ++s) { relax(c, C, ec.data(), rc.data(), t0.data()); ec = t0; }
     }
   } else {
     mg(c, l - 1, rc.data(), ec.data());  // "MG(A_{l-1}, 0, 0, r_{u,l-1}, r_{p,l-1}, l-1)"
   }
   prolong_add(L, ec.data(), x);  // "Correction"
   for (int s = 0; s < c.nu2; ++s) {  // "Relax on u_l and p_l"
-    vanka_sweep(L, x, b, t.data());
+    relax(c, L, x, b, t.data());
     std::copy(t.begin(), t.end(), x);
   }
 }
@@ -652,6 +786,32 @@ void* orc_create(int n_elem, int n_coarse, double nu, double omega, int weightin
   }
   if (!build_coarse(c->lev[0], c->err)) { delete c; return nullptr; }
   return c;
+}
+// Select the V-cycle relaxation (0 Vanka, 1 Braess-Sarazin, 2 Schur-Uzawa) and
+// its parameters; builds D^{-1} and S on every level.  Returns 0 on success.
+int orc_set_relax(void* h, int kind, double t, double omega_r, double omega_j, int nj) {
+  Ctx* c = (Ctx*)h;
+  if (kind < 0 || kind > 2 || t <= 0 || nj < 0) return 1;
+  c->relax = kind;
+  c->t = t;
+  c->omega_r = omega_r;
+  c->omega_j = omega_j;
+  c->nj = nj;
+  if (kind != 0)
+    for (Level& L : c->lev) build_schur(L, t);
+  return 0;
+}
+// one sweep of the configured relaxation on level l
+void orc_relax_sweep(void* h, int l, const double* xin, const double* b, double* xout) {
+  const Ctx& c = *(Ctx*)h;
+  relax(c, c.lev[l], xin, b, xout);
+}
+int64_t orc_schur_nnz(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].S.col.size(); }
+void orc_schur_csr(void* h, int l, int64_t* rowptr, int32_t* col, double* val) {
+  const Csr& S = ((Ctx*)h)->lev[l].S;
+  std::copy(S.rowptr.begin(), S.rowptr.end(), rowptr);
+  std::copy(S.col.begin(), S.col.end(), col);
+  std::copy(S.val.begin(), S.val.end(), val);
 }
 void orc_destroy(void* h) { delete (Ctx*)h; }
 int orc_num_levels(void* h) { return (int)((Ctx*)h)->lev.size(); }
