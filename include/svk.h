@@ -118,10 +118,26 @@ typedef struct svk_config {
                           replicated on every rank (coarse agglomeration); default 64, >= 4 */
   int32_t emul_group;  /* EMULATED transport: id of the in-process group to join */
   int32_t orth;        /* enum svk_orth: FGMRES Gram-Schmidt; default ADAPTIVE */
-  int32_t reserved[2];
+  int32_t relax;         /* enum svk_relax: relaxation inside the V-cycle; default VANKA */
+  int32_t jacobi_sweeps; /* BS / SU: weighted-Jacobi sweeps on S; default 3 */
   uint8_t nccl_id[128]; /* NCCL transport: ncclUniqueId from svk_nccl_unique_id() on rank 0,
                            broadcast to every rank by the caller */
+  double relax_t;        /* BS / SU: t in tD ~ L; default 1 */
+  double relax_omega;    /* BS: omega_BS of alg:bs line 3-4 (unused by SU); default 1 */
+  double jacobi_omega;   /* BS / SU: weight of the Jacobi iteration on S; default 0.8
+                            (SU: 0.4, "optimal Jacobi weight") */
 } svk_config;
+
+/* Relaxation of the V-cycle (alg:mg "Relax on u_l and p_l"):
+ * VANKA           -- additive Vanka (alg:vk), the hot path;
+ * BRAESS_SARAZIN  -- inexact Braess-Sarazin (alg:bs): S dp ~= r_p - (1/t) B D^-1 r_u
+ *                    by jacobi_sweeps weighted-Jacobi sweeps on S = -(1/t) B D^-1 B^T,
+ *                    du = (1/t) D^-1 (r_u - B^T dp), x += relax_omega (du, dp);
+ * SCHUR_UZAWA     -- Schur-Uzawa (alg:uz): du = (1/t) D^-1 r_u,
+ *                    S dp ~= r_p - B du (eq:uzblock; reading 19), x += (du, dp).
+ * D = diag(L) on non-Dirichlet velocity DOFs.  The comparators are single-GPU
+ * (nranks == 1) and exist as the paper's same-run baselines. */
+enum svk_relax { SVK_RELAX_VANKA = 0, SVK_RELAX_BRAESS_SARAZIN = 1, SVK_RELAX_SCHUR_UZAWA = 2 };
 
 /* transports for nranks > 1:
  * NCCL     -- one process per GPU; halos by ncclSend/ncclRecv with the two slab
@@ -214,6 +230,13 @@ int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double*
 /* x = A_0^+ b on level 0 (minimum-norm, reading 3); Dirichlet
  * entries of x set to 0. */
 int svk_coarse_solve(svk_ctx* ctx, const double* b, double* x, void* stream);
+
+/* One sweep of the CONFIGURED relaxation (svk_config.relax) on `level`:
+ * x_out = x_in + correction.  VANKA: identical to svk_vanka_sweep(..., 1, ...);
+ * BRAESS_SARAZIN / SCHUR_UZAWA: alg:bs / alg:uz (see enum svk_relax).
+ * Layout, ownership and stream semantics as svk_vanka_sweep; x_out must not alias
+ * x_in or b.  SVK_ERR_INVALID on a bad level / pointer / aliasing. */
+int svk_relax_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, void* stream);
 
 /* One V(nu_pre, nu_post) cycle (alg:mg) on the finest level; x is
  * in/out (a preconditioner application passes x = 0).  b and x must not alias. */

@@ -21,6 +21,7 @@
 #include "krylov.cuh"
 #include "sweep_fused.cuh"
 #include "residual_strip.cuh"
+#include "relax_bs.cuh"
 #include "dist.cuh"
 
 using namespace svk;
@@ -45,6 +46,9 @@ struct svk_ctx {
   std::vector<BdTile*> d_tiles;  // per level: boundary-patch tiles (k_boundary_patches)
   std::vector<int> ntiles;
   double* d_sw = nullptr;    // extra ping-pong vector for nsweeps > 1, finest-level size
+  // Braess-Sarazin / Schur-Uzawa comparators (relax_bs.cuh)
+  double* d_schur = nullptr;                 // nlev * kSchurStride class stencils of S
+  std::vector<double*> p_rhs, p_dp0, p_dp1;  // per level, pressure-plane sized
   // Krylov
   std::vector<double*> V, Z;
   double* d_w = nullptr;
@@ -401,6 +405,44 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
   return SVK_OK;
 }
 
+// alg:bs / alg:uz sweep (relax_bs.cuh) on level l
+int op_bs(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  const svk_config& c = ctx->cfg;
+  if (x_zero) CK(cudaMemsetAsync(const_cast<double*>(xin), 0, g.len * sizeof(double), s));
+  double* r = ctx->ws_r[l];
+  TRY(op_residual(ctx, l, xin, b, r, s));
+  BsArgs a{};
+  a.g = g;
+  a.inv_t = 1.0 / c.relax_t;
+  a.su = c.relax == SVK_RELAX_SCHUR_UZAWA;
+  a.omega_r = a.su ? 1.0 : c.relax_omega;
+  const FusedFactors& F = ctx->h_fac[l];
+  for (int py = 0; py < 2; ++py)
+    for (int px = 0; px < 2; ++px) a.dinv[py][px] = 1.0 / F.L2D[py][px][2][2];
+  const dim3 pb(32, 4), pg((unsigned)((g.pp + 31) / 32), (unsigned)((g.N + 1 + 3) / 4));
+  k_bs_rhs<<<pg, pb, 0, s>>>(a, r, ctx->p_rhs[l]);
+  CKL();
+  const double* st = ctx->d_schur + (size_t)l * kSchurStride;
+  double* dp = ctx->p_dp0[l];
+  if (c.jacobi_sweeps == 0) CK(cudaMemsetAsync(dp, 0, (size_t)(g.N + 1) * g.pp * sizeof(double), s));
+  for (int k = 0; k < c.jacobi_sweeps; ++k) {
+    double* out = (k & 1) ? ctx->p_dp0[l] : ctx->p_dp1[l];
+    k_schur_jacobi<<<pg, pb, 0, s>>>(g, st, c.jacobi_omega, ctx->p_rhs[l], k == 0 ? nullptr : dp, out);
+    CKL();
+    dp = out;
+  }
+  k_bs_update<<<plane_grid(g), kPlaneBlock, 0, s>>>(a, xin, r, dp, xout);
+  CKL();
+  ctx->launches += 3 + c.jacobi_sweeps;
+  return SVK_OK;
+}
+// "Relax on u_l and p_l" (alg:mg) with the configured relaxation
+int op_relax(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
+  if (ctx->cfg.relax == SVK_RELAX_VANKA) return op_sweep(ctx, l, xin, b, xout, x_zero, s);
+  return op_bs(ctx, l, xin, b, xout, x_zero, s);
+}
+
 int op_restrict(svk_ctx* ctx, int l, const double* rf, double* rc, cudaStream_t s) {
   k_restrict<<<plane_grid(ctx->g[l - 1]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], rf, rc);
   CKL();
@@ -426,9 +468,9 @@ int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
   const LevelGeom& g = ctx->g[0];
   if (ctx->cfg.coarse == SVK_COARSE_SWEEPS3) {
     // three relaxation sweeps from zero, ping-pong x <-> ws_t[0]
-    TRY(op_sweep(ctx, 0, x, b, ctx->ws_t[0], true, s));
-    TRY(op_sweep(ctx, 0, ctx->ws_t[0], b, x, false, s));
-    TRY(op_sweep(ctx, 0, x, b, ctx->ws_t[0], false, s));
+    TRY(op_relax(ctx, 0, x, b, ctx->ws_t[0], true, s));
+    TRY(op_relax(ctx, 0, ctx->ws_t[0], b, x, false, s));
+    TRY(op_relax(ctx, 0, x, b, ctx->ws_t[0], false, s));
     CK(cudaMemcpyAsync(x, ctx->ws_t[0], g.len * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return SVK_OK;
   }
@@ -456,7 +498,7 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
   double* cur = x;
   double* oth = ctx->ws_t[l];
   for (int k = 0; k < ctx->cfg.nu_pre; ++k) {  // "Relax on u_l and p_l"
-    TRY(op_sweep(ctx, l, cur, b, oth, x_zero && k == 0, s));
+    TRY(op_relax(ctx, l, cur, b, oth, x_zero && k == 0, s));
     std::swap(cur, oth);
     if (D) TRY(op_halo(ctx, l, cur, s));
   }
@@ -469,7 +511,7 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
   TRY(op_prolong_add(ctx, l, ctx->ws_x[l - 1], cur, s));       // "Correction"
   if (D) TRY(op_halo(ctx, l, cur, s));
   for (int k = 0; k < ctx->cfg.nu_post; ++k) {                 // "Relax on u_l and p_l"
-    TRY(op_sweep(ctx, l, cur, b, oth, false, s));
+    TRY(op_relax(ctx, l, cur, b, oth, false, s));
     std::swap(cur, oth);
     if (D) TRY(op_halo(ctx, l, cur, s));
   }
@@ -721,6 +763,9 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_bd);
   for (BdTile* p : ctx->d_tiles) F(p);
   F(ctx->d_sw);
+  F(ctx->d_schur);
+  for (auto* v : {&ctx->p_rhs, &ctx->p_dp0, &ctx->p_dp1})
+    for (double* p : *v) F(p);
   for (double* p : ctx->V) F(p);
   for (double* p : ctx->Z) F(p);
   F(ctx->d_w);
@@ -850,6 +895,22 @@ int create_impl(svk_ctx* ctx) {
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
   }
   CK(cudaMalloc(&ctx->d_part, (size_t)(kCgsMax + 1) * kDotBlocks * sizeof(double)));
+  if (c.relax != SVK_RELAX_VANKA) {  // comparator workspaces: S stencils + pressure-plane buffers
+    StencilConst t;
+    if (!build_tables(t, ctx->err)) return SVK_ERR_INVALID;
+    std::vector<double> h((size_t)ctx->nlev * kSchurStride);
+    for (int l = 0; l < ctx->nlev; ++l) build_schur_stencils(t, ctx->g[l].N, c.nu, c.relax_t, &h[(size_t)l * kSchurStride]);
+    CK(cudaMalloc(&ctx->d_schur, h.size() * sizeof(double)));
+    CK(cudaMemcpy(ctx->d_schur, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    for (int l = 0; l < ctx->nlev; ++l) {
+      const int64_t np = (int64_t)(ctx->g[l].N + 1) * ctx->g[l].pp;
+      for (auto* v : {&ctx->p_rhs, &ctx->p_dp0, &ctx->p_dp1}) {
+        double* p;
+        TRY(alloc_vec(ctx, &p, np));
+        v->push_back(p);
+      }
+    }
+  }
   CK(cudaDeviceSynchronize());
   return SVK_OK;
 }
@@ -879,6 +940,11 @@ int svk_config_default(svk_config* cfg, int32_t n_elem) {
   cfg->transport = SVK_TRANSPORT_NONE;
   cfg->agglom_rows = 64;
   cfg->orth = SVK_ORTH_ADAPTIVE;
+  cfg->relax = SVK_RELAX_VANKA;
+  cfg->relax_t = 1.0;
+  cfg->relax_omega = 1.0;
+  cfg->jacobi_omega = 0.8;
+  cfg->jacobi_sweeps = 3;
   return SVK_OK;
 }
 
@@ -897,6 +963,9 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
   if (n != cfg->n_coarse) return SVK_ERR_INVALID;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return SVK_ERR_INVALID;
   if (cfg->orth != SVK_ORTH_ADAPTIVE && cfg->orth != SVK_ORTH_CGS2) return SVK_ERR_INVALID;
+  if (cfg->relax < SVK_RELAX_VANKA || cfg->relax > SVK_RELAX_SCHUR_UZAWA) return SVK_ERR_INVALID;
+  if (cfg->relax != SVK_RELAX_VANKA && (cfg->nranks > 1 || !(cfg->relax_t > 0) || cfg->jacobi_sweeps < 0))
+    return SVK_ERR_INVALID;  // the comparators are single-GPU
   if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
                           (cfg->transport != SVK_TRANSPORT_NCCL && cfg->transport != SVK_TRANSPORT_EMULATED)))
     return SVK_ERR_INVALID;
@@ -1005,6 +1074,19 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
   }
   (void)g;
   return SVK_OK;
+}
+
+int svk_relax_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, void* stream) {
+  TRY(valid_level(ctx, level));
+  TRY(valid_ptr(ctx, x_in, "x_in"));
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, x_out, "x_out"));
+  if (x_in == x_out || b == x_out) {
+    ctx->err = "x_out aliases x_in or b";
+    return SVK_ERR_INVALID;
+  }
+  if (ctx->cfg.relax == SVK_RELAX_VANKA) return svk_vanka_sweep(ctx, level, x_in, b, x_out, 1, stream);
+  return op_bs(ctx, level, x_in, b, x_out, false, (cudaStream_t)stream);
 }
 
 int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream) {

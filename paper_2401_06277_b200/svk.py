@@ -23,6 +23,9 @@ COARSE = {"exact": 0, "sweeps3": 1}
 SWEEP = {"fused": 0, "unfused": 1}
 ORTH = {"adaptive": 0, "cgs2": 1}
 TRANSPORT = {"none": 0, "nccl": 1, "emulated": 2}
+RELAX = {"vanka": 0, "bs": 1, "su": 2}
+# comparator defaults: (t, omega_r, jacobi_omega, jacobi_sweeps)
+RELAX_DEFAULTS = {"bs": (1.0, 1.0, 0.8, 3), "su": (1.0, 1.0, 0.4, 1)}
 
 
 class SvkError(RuntimeError):
@@ -34,7 +37,8 @@ class Config(C.Structure):
                 ("weighting", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("coarse", C.c_int32),
                 ("sweep_impl", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("transport", C.c_int32), ("agglom_rows", C.c_int32), ("emul_group", C.c_int32),
-                ("orth", C.c_int32), ("reserved", C.c_int32 * 2), ("nccl_id", C.c_uint8 * 128)]
+                ("orth", C.c_int32), ("relax", C.c_int32), ("jacobi_sweeps", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+                ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double)]
 
 
 class LevelInfo(C.Structure):
@@ -66,6 +70,7 @@ EXPORTS = {
     "svk_residual": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_matvec": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_vanka_sweep": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "svk_relax_sweep": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_prolong_add": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_coarse_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -146,10 +151,14 @@ class Solver:
                  weighting: str = "mult", nu_pre: int = 1, nu_post: int = 1, coarse: str = "exact",
                  sweep: str = "fused", device: int = 0, rank: int = 0, nranks: int = 1,
                  transport: str = "none", agglom_rows: int = 64, emul_group: int = 0, nccl_id: bytes | None = None,
-                 orth: str = "adaptive"):
+                 orth: str = "adaptive", relax: str = "vanka", relax_t: float | None = None,
+                 relax_omega: float | None = None, jacobi_omega: float | None = None,
+                 jacobi_sweeps: int | None = None):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
-        "emulated" runs nranks logical ranks of one process on one device (one thread each)."""
+        "emulated" runs nranks logical ranks of one process on one device (one thread each).
+        relax: "vanka" (the hot path), "bs" (Braess-Sarazin) or "su" (Schur-Uzawa) comparators;
+        unset comparator parameters take RELAX_DEFAULTS[relax]."""
         import torch
         if not torch.cuda.is_available():
             raise SvkError("libsvk needs a CUDA device (B200, sm_100a); none is visible")
@@ -162,6 +171,13 @@ class Solver:
         cfg.coarse, cfg.sweep_impl, cfg.device = COARSE[coarse], SWEEP[sweep], device
         cfg.rank, cfg.nranks, cfg.transport = rank, nranks, TRANSPORT[transport]
         cfg.agglom_rows, cfg.emul_group, cfg.orth = agglom_rows, emul_group, ORTH[orth]
+        cfg.relax = RELAX[relax]
+        if relax != "vanka":
+            d = RELAX_DEFAULTS[relax]
+            cfg.relax_t = d[0] if relax_t is None else relax_t
+            cfg.relax_omega = d[1] if relax_omega is None else relax_omega
+            cfg.jacobi_omega = d[2] if jacobi_omega is None else jacobi_omega
+            cfg.jacobi_sweeps = d[3] if jacobi_sweeps is None else jacobi_sweeps
         if nccl_id is not None:
             if len(nccl_id) != 128:
                 raise SvkError("nccl_id must be 128 bytes")
@@ -267,6 +283,13 @@ class Solver:
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_vanka_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
                                            self._vec(out, level, "x_out"), nsweeps, _stream(self.torch)))
+        return out
+
+    def relax_sweep(self, level, x, b, out=None):
+        """One sweep of the configured relaxation (svk_relax_sweep)."""
+        out = self.new_vector(level) if out is None else out
+        self._chk(self.lib.svk_relax_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
+                                           self._vec(out, level, "x_out"), _stream(self.torch)))
         return out
 
     def restrict(self, level, rf, out=None):
