@@ -166,9 +166,17 @@ def run_reference(args):
     return 0
 
 
+RELAX_NAMES = {"vanka": "Vanka", "bs": "Braess-Sarazin", "su": "Schur-Uzawa"}
+
+
 def config_dict(args, world=1):
-    return {"workload": "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka"
-                        % (args.n, args.n),
+    relax = getattr(args, "relax", "vanka")
+    if relax == "vanka":
+        wl = "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka" % (args.n, args.n)
+    else:
+        wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-%s"
+              % (args.n, args.n, RELAX_NAMES[relax]))
+    return {"workload": wl, "relaxation": relax,
             "N": args.n, "levels_to": 4, "dofs": n_dof(args.n), "omega_v": 0.8, "weighting": "multiplicity",
             "sweep_impl": args.sweep, "l2": "inputs exceed L2 (%.2f GB per vector vs 126 MB L2)"
             % (n_dof(args.n) * 8 / 1e9),
@@ -211,7 +219,7 @@ def run_svk(args):
         S = Solver(N, sweep=args.sweep, device=dev, rank=rank, nranks=world, transport="nccl",
                    agglom_rows=args.agglom, nccl_id=nid)
     else:
-        S = Solver(N, sweep=args.sweep, device=dev)
+        S = Solver(N, sweep=args.sweep, device=dev, relax=args.relax)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     b, x0 = S.set_problem("mms_paper")
@@ -219,7 +227,7 @@ def run_svk(args):
 
     def step():
         x.copy_(x0)
-        return S.fgmres(b, x, rtol=args.rtol, maxit=200)
+        return S.fgmres(b, x, rtol=args.rtol, maxit=args.maxit)
 
     for _ in range(args.warmup):
         rep, _ = step()
@@ -255,7 +263,9 @@ def run_svk(args):
     value = jobs * n_dof(N) * args.steps / t
     its = [r["iterations"] for r in reps]
 
-    # sweep roofline (dominant kernel)
+    # sweep roofline (dominant kernel); comparator runs have no Vanka sweep to time
+    if nsw == 0:
+        nsw, sw_ms = 1, float("nan")
     t_sweep = sw_ms / 1e3 / max(nsw, 1)
     r0, r1, _ = S.owned_rows()
     share = (r1 - r0) / (N + 1)  # this rank's slab of the sweep (1 on a single GPU)
@@ -318,6 +328,8 @@ def run_svk(args):
                       "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         }
+        if args.relax != "vanka":  # comparator line: no Vanka sweep in it
+            line["sweep"] = line["roofline"] = None
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -333,6 +345,8 @@ def main():
     ap.add_argument("--impl", choices=["svk", "reference"], default="svk")
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--maxit", type=int, default=60,
+                    help="FGMRES iteration cap (no restart: 2 vectors of 1.2 GB per iteration at 4096^2)")
     ap.add_argument("--sweep", choices=["fused", "unfused"], default="fused")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -341,7 +355,11 @@ def main():
     ap.add_argument("--ref-n", type=int, default=256)
     ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs")
     ap.add_argument("--agglom", type=int, default=64)
+    ap.add_argument("--relax", choices=["vanka", "bs", "su"], default="vanka",
+                    help="V-cycle relaxation; bs / su are the paper's same-run comparators (configs[4], 1 GPU)")
     args = ap.parse_args()
+    if args.relax != "vanka" and (args.gpus > 1 or args.impl == "reference"):
+        ap.error("--relax bs/su: single-GPU comparator runs of the svk arm only")
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

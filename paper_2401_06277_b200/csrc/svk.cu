@@ -650,7 +650,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       dlist.assign(hV, hV + m);
       dlist.push_back(ctx->d_w);
       TRY(cgs_dots(ctx, dlist.data(), m + 1, ctx->d_w, S, oraw, s));
-      k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
+      k_scale_coef<<<(m + 63) / 64, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
       CKL();
       TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
@@ -666,7 +666,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       if (ctx->cfg.orth == SVK_ORTH_CGS2 || !(wp2 * kReorthKappa * kReorthKappa >= wn2)) {
         CK(cudaEventRecord(ctx->ev[3], s));
         TRY(cgs_dots(ctx, hV, m, ctx->V[j + 1], S, oraw, s));
-        k_scale_coef<<<1, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
+        k_scale_coef<<<(m + 63) / 64, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
         CKL();
         TRY(cgs_update(ctx, hV, m, o2, ctx->V[j + 1], ctx->V[j + 1], n, S, onrm, s));
         CK(cudaEventRecord(ctx->ev[4], s));

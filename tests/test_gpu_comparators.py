@@ -75,9 +75,10 @@ def test_vcycle_parity(gpu, kind, N):
     assert rel(xg, xo) < 1e-12
 
 
-@pytest.mark.parametrize("kind", ["bs", "su"])
-@pytest.mark.parametrize("N", [16, 64])
+@pytest.mark.parametrize("kind,N", [("bs", 16), ("bs", 64), ("su", 16), ("su", 64), ("su", 128)])
 def test_fgmres_iterations(gpu, kind, N):
+    """SU at 128^2 needs 72 iterations: also the regression test of FGMRES beyond 64
+    basis vectors (the coefficient-scaling launch once covered only 64)."""
     S, O = make(N, kind)
     bg, x0 = S.set_problem("mms_paper")
     rep, _ = S.fgmres(bg, x0, rtol=1e-10, maxit=300)
