@@ -4,23 +4,23 @@
 //
 // Same machinery as the fused Vanka sweep (sweep_fused.cuh): a CTA of 128
 // threads owns a strip of 120 node columns and a chunk of rows, x / p / b rows
-// arrive by TMA into shared-memory rings, and `fused_residual` evaluates the
-// stencil of two lattice rows and one pressure row per step into a residual
-// ring.  The residual ring is then either written out (MODE 0) or restricted on
-// the fly (MODE 1): coarse lattice row C needs fine rows 2C-3 .. 2C+3 (1D Q2
-// interpolation transpose: weights -1/8, 3/8, 1, 3/8, -1/8 around an even coarse
-// index, 3/4, 1, 3/4 around an odd one) and coarse pressure row C' fine rows
-// 2C'-1 .. 2C'+1 (1/2, 1, 1/2), so the fine residual never touches HBM.
+// arrive by TMA into shared-memory rings, and `fused_residual_vals` evaluates the
+// stencil of two lattice rows and one pressure row per step into registers.
+// MODE 0 stores them directly; MODE 1 restricts them on the fly: coarse lattice
+// row C needs fine rows 2C-3 .. 2C+3 (1D Q2 interpolation transpose: weights
+// -1/8, 3/8, 1, 3/8, -1/8 around an even coarse index, 3/4, 1, 3/4 around an odd
+// one) and coarse pressure row C' fine rows 2C'-1 .. 2C'+1 (1/2, 1, 1/2).  The x
+// direction combines a thread's columns with its neighbours' odd columns (one
+// exchange row per step), the y direction accumulates register carries over the
+// coarse rows still open, so the fine residual never touches HBM or a ring.
 #pragma once
 #include "sweep_fused.cuh"
 
 namespace svk {
 
 namespace rz {
-constexpr int RR = 8;                         // residual ring rows (2C-3 .. 2C+3 plus the row being written)
-constexpr int ORS = fz::ORS;
-constexpr int ORP = ORS + RR * 2 * fz::W;
-constexpr int OMB = ORP + 4 * fz::PWID;
+constexpr int ORS = fz::ORS;                  // MODE 1 exchange rows: [step parity][5][128]
+constexpr int OMB = ORS + 2 * 5 * fz::kNT;
 constexpr int kSmemBytes = (OMB + 2) * 8;
 }  // namespace rz
 
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
       tma_load_2d(sm + bprow(spB + 1), &M.bp, kx0 - 2, spB + 1, &bars[0]);
     }
   }
-  auto rrow8 = [&](int j, int c) { return rz::ORS + (j & (rz::RR - 1)) * 2 * fz::W + c * fz::W; };
-  auto rprow4 = [&](int r) { return rz::ORP + (r & 3) * fz::PWID; };
+  double rc_carry[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // MODE 1: open coarse rows sp-1 .. sp+1
+  double pc_carry[2] = {0.0, 0.0};                              // MODE 1: open coarse pressure rows
   for (int sp = spB; sp <= spE; ++sp) {
     const int k = sp - spB;
     mbar_wait(&bars[k & 1], (phases >> (k & 1)) & 1u);
@@ -89,81 +89,85 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
         tma_load_2d(sm + bprow(sp + 2), &M.bp, kx0 - 2, sp + 2, nb);
       }
     }
-    fused_residual<false, NOB, rz::RR, rz::ORS, rz::ORP>(sm, g, F, sp, kx0);
-    __syncthreads();
     if (MODE == 0) {
-      // lattice rows 2sp+1, 2sp+2 and pressure row sp+1, owned columns only;
-      // thread t < 120 owns node column kx0+t = ring columns 2t+4, 2t+5
-      if (t < fz::kNOUT) {
-        const int kx = kx0 + t, i0 = 2 * kx;
-        const double sg = NOB ? -1.0 : 1.0;  // NOB: the ring holds -A x
+      // lattice rows 2sp+1, 2sp+2 and pressure row sp+1 straight from registers:
+      // thread t in [2, 122) owns node column kx0-2+t (lattice columns 2kx, 2kx+1)
+      const ResVals V = fused_residual_vals<false, NOB>(sm, g, F, sp, kx0);
+      const int kx = kx0 - 2 + t, i0 = 2 * kx;
+      if (t >= 2 && t < fz::kNOUT + 2) {
+        const double sg = NOB ? -1.0 : 1.0;  // NOB: the values are -A x
 #pragma unroll
-        for (int rr = 1; rr <= 2; ++rr) {
-          const int j = 2 * sp + rr;
+        for (int rr = 0; rr < 2; ++rr) {
+          const int j = 2 * sp + 1 + rr;
           if (j < 2 * y0 || j >= 2 * y1 || j > lat - 1 || i0 >= g.pu) continue;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const double2 v = lds2(sm + rrow8(j, c) + 2 * t + 4);
+          for (int c = 0; c < 2; ++c)
             *reinterpret_cast<double2*>(R.out + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
-                make_double2(sg * v.x, sg * v.y);
-          }
+                make_double2(sg * V.u[c][2 * rr], sg * V.u[c][2 * rr + 1]);
         }
         const int pr = sp + 1;
-        if (pr >= y0 && pr < y1 && kx < g.pp) R.out[g.op + (int64_t)pr * g.pp + kx] = sg * sm[rprow4(pr) + t + 2];
+        if (pr >= y0 && pr < y1 && kx < g.pp) R.out[g.op + (int64_t)pr * g.pp + kx] = sg * V.p;
       }
+      __syncthreads();  // ring slots of x / p / b are reused by the next prefetch
     } else {
+      // Restriction r_c = P^T r in registers: x first (the odd-column neighbours
+      // come through a small double-buffered exchange row), then y with carries
+      // over the three coarse lattice rows still open (like the sweep's
+      // accumulation).  Thread t in [2, 122) owns coarse lattice column a =
+      // kx0-2+t (its even fine column 2a sits on it) and, for even a, the coarse
+      // pressure column a/2.  1D P^T weights around fine 2C: C even: -1/8, 3/8,
+      // 1, 3/8, -1/8 at offsets -3, -1, 0, 1, 3; C odd: 3/4, 1, 3/4 at -1, 0, 1;
+      // pressure: 1/2, 1, 1/2 around fine node 2C'.
+      const ResVals V = fused_residual_vals<false, NOB>(sm, g, F, sp, kx0);
+      double* xb = sm + rz::ORS + (sp & 1) * 5 * fz::kNT;
+      xb[0 * fz::kNT + t] = V.u[0][1];
+      xb[1 * fz::kNT + t] = V.u[0][3];
+      xb[2 * fz::kNT + t] = V.u[1][1];
+      xb[3 * fz::kNT + t] = V.u[1][3];
+      xb[4 * fz::kNT + t] = V.p;
+      __syncthreads();
       const LevelGeom& gc = R.gc;
-      // coarse lattice row C = sp-1 is complete (fine rows 2C-3 .. 2C+3 = 2sp-5 .. 2sp+1)
-      const int C = sp - 1;
-      if (t < fz::kNOUT && C >= 2 * Y0 && C < 2 * Y1 && C <= gc.lat - 1) {
-        const int c = kx0 + t;  // coarse lattice column; fine columns 2c-3 .. 2c+3 = ring 2t+1 .. 2t+7
-        if (c < gc.pu) {
-          const bool inside = C >= 1 && C <= gc.lat - 2 && c >= 1 && c <= gc.lat - 2;
-          const int ro = (C & 1) ? 1 : 3;  // row offsets -ro .. ro
-          const int co = (c & 1) ? 1 : 3;
+      const int a = kx0 - 2 + t;
+      const int tm1 = max(t - 1, 0), tm2 = max(t - 2, 0), tp1 = min(t + 1, fz::kNT - 1);
+      // y weights of fine rows j0 = 2sp+1 and j1 = 2sp+2 for coarse rows sp-1 .. sp+2
+      const double w_m1 = ((sp - 1) & 1) ? 0.0 : -0.125;  // j0 = 2(sp-1)+3
+      const double w_0 = (sp & 1) ? 0.75 : 0.375;         // j0 = 2sp+1
+      const double w_p1 = ((sp + 1) & 1) ? 0.75 : 0.375;  // j0 = 2(sp+1)-1
+      const double w_p2 = ((sp + 2) & 1) ? 0.0 : -0.125;  // j0 = 2(sp+2)-3
+      const int C = sp - 1;  // coarse lattice row completed by this step
+      const bool emit = t >= 2 && t < fz::kNOUT + 2 && C >= 2 * Y0 && C < 2 * Y1 && C <= gc.lat - 1 && a < gc.pu;
+      const bool inside = C >= 1 && C <= gc.lat - 2 && a >= 1 && a <= gc.lat - 2;
 #pragma unroll
-          for (int comp = 0; comp < 2; ++comp) {
-            double acc = 0.0;
-            if (inside) {
+      for (int comp = 0; comp < 2; ++comp) {
+        double q[2];
 #pragma unroll
-              for (int dy = -3; dy <= 3; ++dy) {
-                if (dy < -ro || dy > ro) continue;
-                // 1D weights of P^T: even coarse index (-1/8, 0, 3/8, 1, 3/8, 0, -1/8); odd (3/4, 1, 3/4)
-                const double wy = (C & 1) ? (dy == 0 ? 1.0 : 0.75)
-                                          : (dy == 0 ? 1.0 : ((dy & 1) ? ((dy == -1 || dy == 1) ? 0.375 : -0.125) : 0.0));
-                if (wy == 0.0) continue;
-                const double* fr = sm + rrow8(2 * C + dy, comp) + 2 * t + 4;  // fine column 2c -> ring 2t+4
-                double sx = 0.0;
-                if (c & 1) {
-                  sx = 0.75 * fr[-1] + fr[0] + 0.75 * fr[1];
-                } else {
-                  sx = -0.125 * fr[-3] + 0.375 * fr[-1] + fr[0] + 0.375 * fr[1] - 0.125 * fr[3];
-                }
-                acc = fma(wy, sx, acc);
-              }
-            }
-            R.out[(comp ? gc.ouy : gc.oux) + (int64_t)C * gc.pu + c] = acc;
-          }
+        for (int rr = 0; rr < 2; ++rr) {
+          const double* ro = xb + (comp * 2 + rr) * fz::kNT;
+          const double e = V.u[comp][2 * rr], o1 = V.u[comp][2 * rr + 1], om1 = ro[tm1];
+          q[rr] = (a & 1) ? e + 0.75 * (om1 + o1) : e + 0.375 * (om1 + o1) - 0.125 * (ro[tm2] + ro[tp1]);
         }
+        const double done = rc_carry[comp][0] + w_m1 * q[0];
+        rc_carry[comp][0] = rc_carry[comp][1] + w_0 * q[0];
+        rc_carry[comp][1] = rc_carry[comp][2] + w_p1 * q[0] + q[1];
+        rc_carry[comp][2] = w_p2 * q[0];
+        if (emit) R.out[(comp ? gc.ouy : gc.oux) + (int64_t)C * gc.pu + a] = inside ? done : 0.0;
       }
-      // coarse pressure row C' = sp/2 (fine rows sp-1 .. sp+1) for even sp
-      if (!(sp & 1)) {
-        const int Cp = sp >> 1;
-        const int cp = (kx0 >> 1) + t;  // coarse node; fine nodes 2cp-1 .. 2cp+1 = r_p ring 2t+1 .. 2t+3
-        if (t < fz::kNOUT / 2 && Cp >= Y0 && Cp < Y1 && Cp <= gc.N && cp < gc.pp) {
-          double acc = 0.0;
-          if (cp <= gc.N) {
-#pragma unroll
-            for (int dy = -1; dy <= 1; ++dy) {
-              const double* fr = sm + rprow4(2 * Cp + dy) + 2 * t + 2;
-              acc = fma(dy ? 0.5 : 1.0, 0.5 * fr[-1] + fr[0] + 0.5 * fr[1], acc);
-            }
-          }
-          R.out[gc.op + (int64_t)Cp * gc.pp + cp] = acc;
+      // pressure: fine node row nr = sp+1
+      {
+        const double qp = (a & 1) ? 0.0 : 0.5 * xb[4 * fz::kNT + tm1] + V.p + 0.5 * xb[4 * fz::kNT + tp1];
+        const int nr = sp + 1;
+        if (!(nr & 1)) {
+          pc_carry[0] += qp;
+        } else {
+          const int Cp = (nr - 1) >> 1, cp = a >> 1;
+          const double done = pc_carry[0] + 0.5 * qp;
+          pc_carry[0] = pc_carry[1] + 0.5 * qp;
+          pc_carry[1] = 0.0;
+          if (!(a & 1) && t >= 2 && t < fz::kNOUT + 2 && Cp >= Y0 && Cp < Y1 && Cp <= gc.N && cp < gc.pp)
+            R.out[gc.op + (int64_t)Cp * gc.pp + cp] = cp <= gc.N ? done : 0.0;
         }
       }
     }
-    __syncthreads();
   }
   mbar_wait(&bars[(spE - spB + 1) & 1], (phases >> ((spE - spB + 1) & 1)) & 1u);
 }

@@ -388,9 +388,13 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) { *reinterpr
 // node (kx0-2+t, sp+1).  Reads x rows 2sp..2sp+4, p rows sp..sp+2, b rows
 // 2sp+1, 2sp+2 (pair sp), b_p row sp+1.  Each stencil coefficient is loaded once
 // and used for both components; the whole 5x5 windows are loaded first.
-template <bool XZERO, bool NOB = false, int RRN = fz::RR, int ORSB = fz::ORS, int ORPB = fz::ORP>
-__device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
-                                               int kx0) {
+struct ResVals {
+  double u[2][4];  // [comp][(j0,c0), (j0,c0+1), (j1,c0), (j1,c0+1)], 0 on Dirichlet / outside points
+  double p;        // pressure residual at node (kx0-2+t, sp+1), 0 outside
+};
+template <bool XZERO, bool NOB = false>
+__device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const LevelGeom& g, const FusedFactors& F,
+                                                       int sp, int kx0) {
   const int N = g.N, lat = g.lat, t = threadIdx.x;
   const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
@@ -489,17 +493,32 @@ __device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, c
              F.GY[0][1][2][1] * Pm[2][2];
   }
   // r = b - A x on non-Dirichlet points (b columns rc0.. = 2t, 2t+1 of the b ring); NOB: b = 0
-  auto rr = [&](int j, int c) { return ORSB + pmod(j, RRN) * 2 * fz::W + c * fz::W; };
+  ResVals R;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
     const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j0, comp) + 2 * t);
     const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j1, comp) + 2 * t);
-    sts2(sm + rr(j0, comp) + 2 * t, (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0,
-         (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0);
-    sts2(sm + rr(j1, comp) + 2 * t, (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0,
-         (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0);
+    R.u[comp][0] = (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0;
+    R.u[comp][1] = (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0;
+    R.u[comp][2] = (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0;
+    R.u[comp][3] = (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0;
   }
-  sm[ORPB + (nrow & 3) * fz::PWID + t] = pok ? (NOB ? 0.0 : sm[bprow(nrow) + t]) - bu : 0.0;
+  R.p = pok ? (NOB ? 0.0 : sm[bprow(nrow) + t]) - bu : 0.0;
+  return R;
+}
+// the same, stored into the residual rings (rows j0, j1 and pressure row sp+1)
+template <bool XZERO, bool NOB = false, int RRN = fz::RR, int ORSB = fz::ORS, int ORPB = fz::ORP>
+__device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
+                                               int kx0) {
+  const ResVals R = fused_residual_vals<XZERO, NOB>(sm, g, F, sp, kx0);
+  const int t = threadIdx.x, j0 = 2 * sp + 1, j1 = 2 * sp + 2;
+  auto rr = [&](int j, int c) { return ORSB + pmod(j, RRN) * 2 * fz::W + c * fz::W; };
+#pragma unroll
+  for (int comp = 0; comp < 2; ++comp) {
+    sts2(sm + rr(j0, comp) + 2 * t, R.u[comp][0], R.u[comp][1]);
+    sts2(sm + rr(j1, comp) + 2 * t, R.u[comp][2], R.u[comp][3]);
+  }
+  sm[ORPB + ((sp + 1) & 3) * fz::PWID + t] = R.p;
 }
 
 // forward even/odd transform of one 5-vector with stride st (in place)
