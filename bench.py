@@ -330,6 +330,8 @@ def run_svk(args):
         }
         if args.relax != "vanka":  # comparator line: no Vanka sweep in it
             line["sweep"] = line["roofline"] = None
+        elif args.sweep != "fused":  # comparator line: the roofline accounting is the fused kernel's
+            line["roofline"] = None
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -347,7 +349,8 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--maxit", type=int, default=60,
                     help="FGMRES iteration cap (no restart: 2 vectors of 1.2 GB per iteration at 4096^2)")
-    ap.add_argument("--sweep", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--sweep", choices=["fused", "unfused", "simple"], default="fused",
+                    help="unfused / simple (per-patch stored inverses, N <= 2048): the paper's split kernels, comparators")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -97,7 +97,12 @@ enum svk_problem { SVK_PROBLEM_ZERO = 0, SVK_PROBLEM_MMS_PAPER = 1, SVK_PROBLEM_
  * UNFUSED -- residual, per-patch solve into a packed buffer, gather update
  *            (the paper's form/apply/update kernel split), kept as a
  *            cross-check of the fused kernel. */
-enum svk_sweep_impl { SVK_SWEEP_FUSED = 0, SVK_SWEEP_UNFUSED = 1 };
+enum svk_sweep_impl { SVK_SWEEP_FUSED = 0, SVK_SWEEP_UNFUSED = 1, SVK_SWEEP_SIMPLE = 2 };
+/* SIMPLE -- the paper's "simple Vanka" baseline: every patch's
+ *           inverse is built and stored at svk_create (51 x 51 doubles per patch
+ *           and level, about 28 KB per fine-grid node over the hierarchy: N <= 2048
+ *           on one B200; larger N returns SVK_ERR_CUDA from svk_create), applied by
+ *           the unfused kernel split.  Comparator only; same arithmetic as alg:vk. */
 
 typedef struct svk_config {
   int32_t n_elem;     /* N, elements per side of the finest grid; N = n_coarse * 2^k */

@@ -419,6 +419,85 @@ __global__ void k_patch_setup(const int* __restrict__ Ns, double nu, double* __r
 }
 
 // ---------------------------------------------------------------------------
+// Simple Vanka (the paper's baseline variant):
+// every patch builds and inverts its own A_i and stores it, instead of the 25
+// shared group inverses of tuned Vanka.  One CTA per patch (batched fp64
+// Gauss-Jordan, as k_patch_setup); the inverse is stored slot-interleaved over
+// the patches, inv[(r * 51 + c) * np + p], so that the apply kernel's per-patch
+// reads are coalesced across the threads of a warp.
+// ---------------------------------------------------------------------------
+__global__ void k_patch_setup_simple(LevelGeom g, double nu, int64_t p0, double* __restrict__ inv_out,
+                                     int* __restrict__ status) {
+  const int N = g.N, lat = g.lat;
+  const int64_t np = (int64_t)(N + 1) * (N + 1);
+  const int64_t p = p0 + blockIdx.x;
+  if (p >= np) return;
+  const int kx = (int)(p % (N + 1)), ky = (int)(p / (N + 1));
+  __shared__ double a[kSlots * kSlots];
+  __shared__ double colk[kSlots];
+  __shared__ int slot[kSlots], perm[kSlots];
+  __shared__ Dof dof[kSlots];
+  __shared__ int n, flag;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int comp = 0; comp < 2; ++comp)
+      for (int oy = 0; oy < 5; ++oy)
+        for (int ox = 0; ox < 5; ++ox) {
+          const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+          if (i < 1 || j < 1 || i > lat - 2 || j > lat - 2) continue;
+          dof[m] = Dof{comp, i, j};
+          slot[m] = comp * 25 + oy * 5 + ox;
+          ++m;
+        }
+    dof[m] = Dof{2, kx, ky};
+    slot[m] = 50;
+    n = m + 1;
+    flag = 0;
+  }
+  __syncthreads();
+  const int nn = n;
+  for (int q = threadIdx.x; q < nn * nn; q += blockDim.x) a[q] = a_entry(dof[q / nn], dof[q % nn], N, nu, g.h);
+  __syncthreads();
+  const bool ok = gj_invert(a, nn, nn, perm, colk, &flag);
+  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) inv_out[(int64_t)q * np + p] = 0.0;
+  __syncthreads();
+  if (!ok) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  for (int q = threadIdx.x; q < nn * nn; q += blockDim.x)
+    inv_out[(int64_t)(slot[q / nn] * kSlots + slot[q % nn]) * np + p] = a[q];
+}
+// delta_p = A_p^{-1} V_p r with patch p's own stored inverse (one thread per patch)
+__global__ void __launch_bounds__(128) k_patch_solve_simple(LevelGeom g, const double* __restrict__ r,
+                                                            const double* __restrict__ inv,
+                                                            double* __restrict__ dbuf) {
+  const int N = g.N, lat = g.lat;
+  const int64_t np = (int64_t)(N + 1) * (N + 1);
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const int kx = (int)(p % (N + 1)), ky = (int)(p / (N + 1));
+  double rv[kSlots];
+#pragma unroll
+  for (int comp = 0; comp < 2; ++comp)
+#pragma unroll
+    for (int oy = 0; oy < 5; ++oy)
+#pragma unroll
+      for (int ox = 0; ox < 5; ++ox) {
+        const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+        const bool ok = i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2;
+        rv[comp * 25 + oy * 5 + ox] = ok ? r[(comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i] : 0.0;
+      }
+  rv[50] = r[p_at(g, kx, ky)];
+  for (int s = 0; s < kSlots; ++s) {
+    double d = 0.0;
+#pragma unroll
+    for (int t = 0; t < kSlots; ++t) d = fma(__ldcs(inv + (int64_t)(s * kSlots + t) * np + p), rv[t], d);
+    dbuf[(int64_t)s * np + p] = d;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Level-0 minimum-norm solve (reading 3).  Setup builds the bordered
 // matrix [[A_II, n],[n^T, 0]] (n = constant pressure / sqrt(m)) in global
 // memory and inverts it with one CTA; the top-left block is pinv(A_II).

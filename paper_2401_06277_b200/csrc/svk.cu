@@ -42,6 +42,7 @@ struct svk_ctx {
   // per-level workspaces
   std::vector<double*> ws_x, ws_t, ws_r, ws_b;
   double* d_dbuf = nullptr;  // packed patch buffer (unfused sweep), finest-level size
+  std::vector<double*> d_inv_simple;  // SIMPLE: per level, every patch's inverse (slot-interleaved)
   double* d_bd = nullptr;    // boundary-patch corrections (fused sweep), finest-level size
   std::vector<BdTile*> d_tiles;  // per level: boundary-patch tiles (k_boundary_patches)
   std::vector<int> ntiles;
@@ -397,8 +398,11 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
   }
   TRY(op_residual(ctx, l, xin, b, r, s));
   const int64_t np = (int64_t)(g.N + 1) * (g.N + 1);
-  k_patch_solve_unfused<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(g, r, ctx->d_inv + (size_t)l * 25 * kGroupStride,
-                                                                     ctx->d_dbuf);
+  if (ctx->cfg.sweep_impl == SVK_SWEEP_SIMPLE)
+    k_patch_solve_simple<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(g, r, ctx->d_inv_simple[l], ctx->d_dbuf);
+  else
+    k_patch_solve_unfused<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(g, r, ctx->d_inv + (size_t)l * 25 * kGroupStride,
+                                                                       ctx->d_dbuf);
   CKL();
   k_vanka_update<<<plane_grid(g), kPlaneBlock, 0, s>>>(g, ctx->cfg.omega_v, scalar_w, xin, ctx->d_dbuf, xout);
   CKL();
@@ -760,6 +764,7 @@ int free_ctx(svk_ctx* ctx) {
   for (auto* v : {&ctx->ws_x, &ctx->ws_t, &ctx->ws_r, &ctx->ws_b})
     for (double* p : *v) F(p);
   F(ctx->d_dbuf);
+  for (double* p : ctx->d_inv_simple) F(p);
   F(ctx->d_bd);
   for (BdTile* p : ctx->d_tiles) F(p);
   F(ctx->d_sw);
@@ -890,7 +895,33 @@ int create_impl(svk_ctx* ctx) {
     ctx->ntiles.push_back((int)t.size());
     CK(cudaMemcpy(d, t.data(), t.size() * sizeof(BdTile), cudaMemcpyHostToDevice));
   }
-  if (c.sweep_impl == SVK_SWEEP_UNFUSED) {
+  if (c.sweep_impl == SVK_SWEEP_SIMPLE) {  // simple Vanka: build and store every patch's inverse
+    int* d_st;
+    CK(cudaMalloc(&d_st, sizeof(int)));
+    CK(cudaMemset(d_st, 0, sizeof(int)));
+    for (int l = 0; l < ctx->nlev; ++l) {
+      const int64_t np = (int64_t)(ctx->g[l].N + 1) * (ctx->g[l].N + 1);
+      double* p = nullptr;
+      if (cudaMalloc(&p, (size_t)np * kGroupStride * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(d_st);
+        ctx->err = "simple Vanka: per-patch inverses do not fit in device memory";
+        return SVK_ERR_CUDA;
+      }
+      ctx->d_inv_simple.push_back(p);
+      for (int64_t p0 = 0; p0 < np; p0 += (1 << 30))
+        k_patch_setup_simple<<<(unsigned)std::min<int64_t>(np - p0, 1 << 30), 128>>>(ctx->g[l], c.nu, p0, p, d_st);
+      CKL();
+    }
+    int hst = 0;
+    CK(cudaMemcpy(&hst, d_st, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d_st);
+    if (hst) {
+      ctx->err = "simple Vanka: singular patch matrix";
+      return SVK_ERR_SINGULAR;
+    }
+  }
+  if (c.sweep_impl == SVK_SWEEP_UNFUSED || c.sweep_impl == SVK_SWEEP_SIMPLE) {
     const LevelGeom& gf = ctx->g.back();
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
   }
@@ -964,6 +995,7 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return SVK_ERR_INVALID;
   if (cfg->orth != SVK_ORTH_ADAPTIVE && cfg->orth != SVK_ORTH_CGS2) return SVK_ERR_INVALID;
   if (cfg->relax < SVK_RELAX_VANKA || cfg->relax > SVK_RELAX_SCHUR_UZAWA) return SVK_ERR_INVALID;
+  if (cfg->sweep_impl < SVK_SWEEP_FUSED || cfg->sweep_impl > SVK_SWEEP_SIMPLE) return SVK_ERR_INVALID;
   if (cfg->relax != SVK_RELAX_VANKA && (cfg->nranks > 1 || !(cfg->relax_t > 0) || cfg->jacobi_sweeps < 0))
     return SVK_ERR_INVALID;  // the comparators are single-GPU
   if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
@@ -1057,7 +1089,7 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
   }
   cudaStream_t s = (cudaStream_t)stream;
   const LevelGeom& g = ctx->g[level];
-  if (ctx->cfg.sweep_impl == SVK_SWEEP_UNFUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
+  if (ctx->cfg.sweep_impl != SVK_SWEEP_FUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
   TRY(op_halo(ctx, level, const_cast<double*>(b), s));
   TRY(op_halo(ctx, level, const_cast<double*>(x_in), s));
   if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);

@@ -20,7 +20,7 @@ SVK_OK, SVK_NOT_CONVERGED = 0, 1
 PROBLEMS = {"zero": 0, "mms_paper": 1, "mms_inspace": 2, "cavity": 3}
 WEIGHTING = {"mult": 0, "scalar": 1}
 COARSE = {"exact": 0, "sweeps3": 1}
-SWEEP = {"fused": 0, "unfused": 1}
+SWEEP = {"fused": 0, "unfused": 1, "simple": 2}
 ORTH = {"adaptive": 0, "cgs2": 1}
 TRANSPORT = {"none": 0, "nccl": 1, "emulated": 2}
 RELAX = {"vanka": 0, "bs": 1, "su": 2}

@@ -12,7 +12,7 @@ import svk_inputs
 
 pytestmark = pytest.mark.gpu
 
-IMPLS = ["fused", "unfused"]
+IMPLS = ["fused", "unfused", "simple"]  # simple: per-patch stored inverses (NEXT-3)
 
 
 def rel(a, b):
