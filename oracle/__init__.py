@@ -28,6 +28,7 @@ _lib = None
 
 MMS_ZERO, MMS_PAPER, MMS_INSPACE, CAVITY = 0, 1, 2, 3
 RELAX_VANKA, RELAX_BS, RELAX_SU = 0, 1, 2
+PRECOND_MG, PRECOND_BT = 0, 1
 WEIGHT_MULT, WEIGHT_SCALAR = 0, 1
 
 
@@ -82,6 +83,10 @@ def _load():
             "orc_relax_sweep": (None, [P, I, P, P, P]),
             "orc_schur_nnz": (I64, [P, I]),
             "orc_schur_csr": (None, [P, I, P, P, P]),
+            "orc_set_precond": (I, [P, I, I, I, D, D]),
+            "orc_precond_apply": (None, [P, P, P]),
+            "orc_mass_nnz": (I64, [P, I]),
+            "orc_mass_csr": (None, [P, I, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -264,6 +269,29 @@ class Oracle:
         col = np.zeros(nnz, np.int32)
         val = np.zeros(nnz, np.float64)
         self._lib.orc_schur_csr(self._h, level, _ptr(rp), _ptr(col), _ptr(val))
+        return sp.csr_matrix((val, col, rp), shape=(n, n))
+
+    def set_precond(self, kind: int, cycles: int = 3, nu: int = 3, omega_u: float = 1.0, omega_p: float = 0.6):
+        """FGMRES preconditioner: PRECOND_MG (monolithic V-cycle) or PRECOND_BT (block-triangular,
+        alg:bt: `cycles` V(nu,nu) cycles of weighted Jacobi on M (omega_p) then on L (omega_u))."""
+        if self._lib.orc_set_precond(self._h, kind, cycles, nu, omega_u, omega_p) != 0:
+            raise ValueError("oracle: bad preconditioner parameters")
+
+    def precond_apply(self, r) -> np.ndarray:
+        r = _f64(r)
+        z = np.zeros_like(r)
+        self._lib.orc_precond_apply(self._h, _ptr(r), _ptr(z))
+        return z
+
+    def mass(self, level: int):
+        """Q1 pressure mass matrix (after set_precond(PRECOND_BT))."""
+        import scipy.sparse as sp
+        n = (self.N(level) + 1) ** 2
+        nnz = int(self._lib.orc_mass_nnz(self._h, level))
+        rp = np.zeros(n + 1, np.int64)
+        col = np.zeros(nnz, np.int32)
+        val = np.zeros(nnz, np.float64)
+        self._lib.orc_mass_csr(self._h, level, _ptr(rp), _ptr(col), _ptr(val))
         return sp.csr_matrix((val, col, rp), shape=(n, n))
 
     def restrict(self, level: int, rf) -> np.ndarray:

@@ -80,6 +80,12 @@ struct Level {
   std::vector<double> Dinv;
   Csr S;
   std::vector<double> Sdiag;
+  // Block-triangular preconditioner (alg:bt): Q1 pressure mass matrix
+  // M_kl = int phi_l phi_k (pressure indices), and on level 0 dense LU factors of
+  // the velocity block of A (Dirichlet rows are identity rows) and of M.
+  Csr Mp;
+  std::vector<double> lu_u, lu_m;
+  std::vector<int> piv_u, piv_m;
   // level-0 direct solve (reading 3: minimum-norm)
   std::vector<int64_t> interior;
   std::vector<double> clu;
@@ -98,6 +104,10 @@ struct Ctx {
   int relax = 0;
   double t = 1.0, omega_r = 1.0, omega_j = 0.8;
   int nj = 3;
+  // FGMRES preconditioner: 0 monolithic V-cycle (alg:mg), 1 block-triangular
+  // (alg:bt) with bt_cycles V(bt_nu, bt_nu) cycles of weighted Jacobi per block
+  int precond = 0, bt_cycles = 3, bt_nu = 3;
+  double bt_omega_u = 1.0, bt_omega_p = 0.6;
   std::vector<Level> lev;
   std::string err;
 };
@@ -731,6 +741,154 @@ void mg(const Ctx& c, int l, const double* b, double* x) {
   }
 }
 
+// --------------------------------------------------------------------------
+// Block-triangular preconditioner (alg:bt) for the comparison of
+// the upper block-triangular system [[L, B^T],[0, -M]] (d_u, d_p) = r
+// with M the Q1 pressure mass matrix (Shat ~ -M), each block inverted
+// approximately by multigrid V-cycles with weighted-Jacobi smoothing (P:647-649:
+// 3 V(3,3) cycles per block, Jacobi weights 0.6 (pressure) and 1.0 (velocity)).
+// Block "part" 0 = the velocity block of the interior system (both components;
+// corrections vanish on Dirichlet DOFs), part 1 = M.  Vectors are full-length; the other part is 0.
+// --------------------------------------------------------------------------
+void assemble_mass(Level& L) {
+  const int N = L.N;
+  const double h = L.h;
+  double Me[4][4] = {{0}};
+  for (int qx = 0; qx < 3; ++qx)
+    for (int qy = 0; qy < 3; ++qy) {
+      const double t = kGP[qx], sy = kGP[qy], w = kGW[qx] * kGW[qy] * h * h;
+      double phi[4];
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) phi[d * 2 + c] = q1(c, t) * q1(d, sy);
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) Me[a][b] += w * phi[a] * phi[b];
+    }
+  std::vector<std::map<int32_t, double>> rows(L.np);
+  for (int ey = 0; ey < N; ++ey)
+    for (int ex = 0; ex < N; ++ex) {
+      int64_t pi[4];
+      for (int d = 0; d < 2; ++d)
+        for (int c = 0; c < 2; ++c) pi[d * 2 + c] = (int64_t)(ey + d) * L.npn + ex + c;
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) rows[pi[a]][(int32_t)pi[b]] += Me[a][b];
+    }
+  L.Mp = Csr();
+  L.Mp.nrows = L.np;
+  L.Mp.rowptr.assign(L.np + 1, 0);
+  for (int64_t k = 0; k < L.np; ++k) {
+    for (auto& kv : rows[k]) {
+      L.Mp.col.push_back(kv.first);
+      L.Mp.val.push_back(kv.second);
+    }
+    L.Mp.rowptr[k + 1] = (int64_t)L.Mp.col.size();
+  }
+}
+// r = b - A_part x on the part's range (velocity: 0 on Dirichlet rows)
+void blk_residual(const Level& L, int part, const double* x, const double* b, double* r) {
+  const int64_t nvel = 2 * L.nv;
+  if (part == 0) {
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < nvel; ++q) {
+      double s = b[q];
+      for (int64_t k = L.A.rowptr[q]; k < L.A.rowptr[q + 1]; ++k)
+        if (L.A.col[k] < nvel) s -= L.A.val[k] * x[L.A.col[k]];
+      r[q] = L.dir[q] ? 0.0 : s;
+    }
+  } else {
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < L.np; ++k) {
+      double s = b[nvel + k];
+      for (int64_t q = L.Mp.rowptr[k]; q < L.Mp.rowptr[k + 1]; ++q) s -= L.Mp.val[q] * x[nvel + L.Mp.col[q]];
+      r[nvel + k] = s;
+    }
+  }
+}
+double blk_diag(const Level& L, int part, int64_t g) {
+  const int64_t nvel = 2 * L.nv;
+  if (part == 0) {
+    for (int64_t k = L.A.rowptr[g]; k < L.A.rowptr[g + 1]; ++k)
+      if (L.A.col[k] == g) return L.A.val[k];
+    return 1.0;
+  }
+  for (int64_t q = L.Mp.rowptr[g - nvel]; q < L.Mp.rowptr[g - nvel + 1]; ++q)
+    if (L.Mp.col[q] == g - nvel) return L.Mp.val[q];
+  return 1.0;
+}
+// one weighted-Jacobi sweep x <- x + omega D^{-1} (b - A_part x)
+void blk_jacobi(const Level& L, int part, double omega, double* x, const double* b) {
+  std::vector<double> r(L.ntot, 0.0);
+  blk_residual(L, part, x, b, r.data());
+  const int64_t lo = part == 0 ? 0 : 2 * L.nv, hi = part == 0 ? 2 * L.nv : L.ntot;
+  for (int64_t g = lo; g < hi; ++g) x[g] += omega * r[g] / blk_diag(L, part, g);
+}
+bool build_block_coarse(Level& L, std::string& err) {
+  const int64_t nvel = 2 * L.nv;
+  // the interior velocity system: identity rows at Dirichlet DOFs, Dirichlet columns dropped
+  L.lu_u.assign((size_t)nvel * nvel, 0.0);
+  for (int64_t r = 0; r < nvel; ++r) {
+    if (L.dir[r]) {
+      L.lu_u[(size_t)r * nvel + r] = 1.0;
+      continue;
+    }
+    for (int64_t k = L.A.rowptr[r]; k < L.A.rowptr[r + 1]; ++k)
+      if (L.A.col[k] < nvel && !L.dir[L.A.col[k]]) L.lu_u[(size_t)r * nvel + L.A.col[k]] = L.A.val[k];
+  }
+  L.lu_m.assign((size_t)L.np * L.np, 0.0);
+  for (int64_t r = 0; r < L.np; ++r)
+    for (int64_t q = L.Mp.rowptr[r]; q < L.Mp.rowptr[r + 1]; ++q) L.lu_m[(size_t)r * L.np + L.Mp.col[q]] = L.Mp.val[q];
+  if (!lu_factor(L.lu_u, L.piv_u, (int)nvel) || !lu_factor(L.lu_m, L.piv_m, (int)L.np)) {
+    err = "singular block on level 0";
+    return false;
+  }
+  return true;
+}
+// scalar V(nu, nu) cycle (alg:mg with a Jacobi smoother) for block `part` on level l
+void blk_mg(const Ctx& c, int l, int part, const double* b, double* x) {
+  const Level& L = c.lev[l];
+  const int64_t nvel = 2 * L.nv;
+  const int64_t lo = part == 0 ? 0 : nvel, hi = part == 0 ? nvel : L.ntot;
+  if (l == 0) {
+    std::vector<double> v(b + lo, b + hi);
+    if (part == 0) lu_solve(L.lu_u, L.piv_u, (int)nvel, v.data());
+    else lu_solve(L.lu_m, L.piv_m, (int)L.np, v.data());
+    std::copy(v.begin(), v.end(), x + lo);
+    return;
+  }
+  const double w = part == 0 ? c.bt_omega_u : c.bt_omega_p;
+  for (int s = 0; s < c.bt_nu; ++s) blk_jacobi(L, part, w, x, b);
+  std::vector<double> r(L.ntot, 0.0);
+  blk_residual(L, part, x, b, r.data());
+  const Level& C = c.lev[l - 1];
+  std::vector<double> rc(C.ntot), ec(C.ntot, 0.0);
+  restrict_(C, L, r.data(), rc.data());
+  blk_mg(c, l - 1, part, rc.data(), ec.data());
+  prolong_add(L, ec.data(), x);
+  for (int s = 0; s < c.bt_nu; ++s) blk_jacobi(L, part, w, x, b);
+}
+// z = BT(r): alg:bt lines 1-2 (the updates of lines 3-4 are z itself)
+void bt_apply(const Ctx& c, const double* r, double* z) {
+  const Level& L = c.lev.back();
+  const int l = (int)c.lev.size() - 1;
+  const int64_t nvel = 2 * L.nv;
+  std::vector<double> rhs(L.ntot, 0.0);
+  std::fill(z, z + L.ntot, 0.0);
+  for (int64_t k = 0; k < L.np; ++k) rhs[nvel + k] = -r[nvel + k];       // M dp = -r_p
+  for (int it = 0; it < c.bt_cycles; ++it) blk_mg(c, l, 1, rhs.data(), z);
+  std::vector<double> btdp(nvel);
+  apply_BT(L, z + nvel, btdp.data());
+  for (int64_t j = 0; j < nvel; ++j) rhs[j] = L.dir[j] ? 0.0 : r[j] - btdp[j];  // L du = r_u - B^T dp
+  for (int64_t k = 0; k < L.np; ++k) rhs[nvel + k] = 0.0;
+  for (int it = 0; it < c.bt_cycles; ++it) blk_mg(c, l, 0, rhs.data(), z);
+}
+// FGMRES preconditioner z = M r
+void precond_apply(const Ctx& c, const double* r, double* z) {
+  if (c.precond == 1) bt_apply(c, r, z);
+  else {
+    std::fill(z, z + c.lev.back().ntot, 0.0);
+    mg(c, (int)c.lev.size() - 1, r, z);
+  }
+}
+
 // deterministic blocked dot product (fixed 4096-element blocks)
 double dot(const double* a, const double* b, int64_t n) {
   const int64_t B = 4096;
@@ -805,6 +963,29 @@ int orc_set_relax(void* h, int kind, double t, double omega_r, double omega_j, i
 void orc_relax_sweep(void* h, int l, const double* xin, const double* b, double* xout) {
   const Ctx& c = *(Ctx*)h;
   relax(c, c.lev[l], xin, b, xout);
+}
+// FGMRES preconditioner: 0 monolithic V-cycle, 1 block-triangular (alg:bt)
+int orc_set_precond(void* h, int kind, int cycles, int nu, double omega_u, double omega_p) {
+  Ctx* c = (Ctx*)h;
+  if (kind < 0 || kind > 1 || cycles < 1 || nu < 0) return 1;
+  c->precond = kind;
+  c->bt_cycles = cycles;
+  c->bt_nu = nu;
+  c->bt_omega_u = omega_u;
+  c->bt_omega_p = omega_p;
+  if (kind == 1) {
+    for (Level& L : c->lev) assemble_mass(L);
+    if (!build_block_coarse(c->lev[0], c->err)) return 2;
+  }
+  return 0;
+}
+void orc_precond_apply(void* h, const double* r, double* z) { precond_apply(*(Ctx*)h, r, z); }
+int64_t orc_mass_nnz(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].Mp.col.size(); }
+void orc_mass_csr(void* h, int l, int64_t* rowptr, int32_t* col, double* val) {
+  const Csr& M = ((Ctx*)h)->lev[l].Mp;
+  std::copy(M.rowptr.begin(), M.rowptr.end(), rowptr);
+  std::copy(M.col.begin(), M.col.end(), col);
+  std::copy(M.val.begin(), M.val.end(), val);
 }
 int64_t orc_schur_nnz(void* h, int l) { return (int64_t)((Ctx*)h)->lev[l].S.col.size(); }
 void orc_schur_csr(void* h, int l, int64_t* rowptr, int32_t* col, double* val) {
@@ -968,7 +1149,7 @@ int orc_fgmres(void* h, const double* b, double* x, double rtol, int maxit, doub
   bool conv = false;
   for (int j = 0; j < maxit; ++j) {
     Z.emplace_back(n, 0.0);
-    mg(c, (int)c.lev.size() - 1, V[j].data(), Z[j].data());  // z_j = M v_j
+    precond_apply(c, V[j].data(), Z[j].data());              // z_j = M v_j
     std::vector<double> w(n);
     matvec_masked(L, Z[j].data(), w.data());                  // w = A z_j
     for (int i = 0; i <= j; ++i) {                            // modified Gram-Schmidt

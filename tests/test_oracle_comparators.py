@@ -144,3 +144,60 @@ def test_comparator_iteration_counts_oracle_internal():
         assert np.abs(x[: 2 * nv] - ex[: 2 * nv]).max() < 1e-9
         its[name] = k
     assert its == {"bs": 14, "su": 31}
+
+
+# ------------------------------------------------- block-triangular preconditioner (alg:bt)
+def q1_mass_1d(N):
+    """1D Q1 mass matrix by exact polynomial integration (brute.Q1 bases)."""
+    h = 1.0 / N
+    me = np.array([[brute._int01(a * b) * h for b in brute.Q1] for a in brute.Q1])
+    m = np.zeros((N + 1, N + 1))
+    for e in range(N):
+        m[e:e + 2, e:e + 2] += me
+    return m
+
+
+@pytest.mark.parametrize("N", [4, 8])
+def test_pressure_mass_matrix_is_q1_kronecker(N):
+    o = oracle.Oracle(N, n_coarse=4)
+    o.set_precond(oracle.PRECOND_BT)
+    m = q1_mass_1d(N)
+    assert rel(o.mass(o.fine).toarray(), np.kron(m, m)) < 1e-14
+
+
+@pytest.mark.parametrize("N", [8, 16])
+def test_bt_many_cycles_is_exact_upper_block_triangular_solve(N):
+    """alg:bt with converged block solves = [[L, B^T],[0, -M]]^{-1} r (eq:schuruzawablock,
+    P:343-357) on the interior system; dense brute-force L, B and Q1 mass."""
+    o = oracle.Oracle(N)
+    o.set_precond(oracle.PRECOND_BT, cycles=60, nu=3, omega_u=1.0, omega_p=0.6)
+    A = brute.full_operator(N)
+    d = brute.dirichlet(N)
+    nvel = 2 * (2 * N + 1) ** 2
+    fu = ~d[:nvel]
+    m = q1_mass_1d(N)
+    M = np.kron(m, m)
+    L = A[:nvel, :nvel][np.ix_(fu, fu)]
+    BT = A[:nvel, nvel:][fu]
+    K = np.block([[L, BT], [np.zeros((M.shape[0], L.shape[0])), -M]])
+    r = svk_inputs.random_vector(N, 11)
+    r[d] = 0.0
+    z = o.precond_apply(r)
+    want = np.linalg.solve(K, np.concatenate([r[:nvel][fu], r[nvel:]]))
+    assert np.all(z[:nvel][~fu] == 0)
+    assert rel(np.concatenate([z[:nvel][fu], z[nvel:]]), want) < 1e-11
+
+
+def test_bt_linear_and_fgmres_oracle_internal():
+    o = oracle.Oracle(16)
+    o.set_precond(oracle.PRECOND_BT)
+    r = svk_inputs.random_vector(16, 12)
+    r[o.dirichlet(o.fine)] = 0.0
+    assert rel(o.precond_apply(-2.0 * r), -2.0 * o.precond_apply(r)) < 1e-14
+    b, x0 = o.problem(oracle.MMS_PAPER)
+    x, k, _, tr, st = o.fgmres(b, x0, rtol=1e-10, maxit=200)
+    assert st == 0 and tr < 1e-9
+    ex = o.exact(oracle.MMS_PAPER)
+    nv = (2 * 16 + 1) ** 2
+    assert np.abs(x[: 2 * nv] - ex[: 2 * nv]).max() < 1e-9
+    assert k == 18  # oracle-internal regression (3 V(3,3) per block, omega 1.0 / 0.6, P:647-649)
