@@ -171,7 +171,11 @@ RELAX_NAMES = {"vanka": "Vanka", "bs": "Braess-Sarazin", "su": "Schur-Uzawa"}
 
 def config_dict(args, world=1):
     relax = getattr(args, "relax", "vanka")
-    if relax == "vanka":
+    if getattr(args, "precond", "mg") == "bt":
+        wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10) + block-triangular "
+              "preconditioner (3 V(3,3) Jacobi cycles per block)" % (args.n, args.n))
+        relax = "block-triangular"
+    elif relax == "vanka":
         wl = "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka" % (args.n, args.n)
     else:
         wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-%s"
@@ -219,7 +223,7 @@ def run_svk(args):
         S = Solver(N, sweep=args.sweep, device=dev, rank=rank, nranks=world, transport="nccl",
                    agglom_rows=args.agglom, nccl_id=nid)
     else:
-        S = Solver(N, sweep=args.sweep, device=dev, relax=args.relax)
+        S = Solver(N, sweep=args.sweep, device=dev, relax=args.relax, precond=args.precond)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     b, x0 = S.set_problem("mms_paper")
@@ -328,7 +332,7 @@ def run_svk(args):
                       "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         }
-        if args.relax != "vanka":  # comparator line: no Vanka sweep in it
+        if args.relax != "vanka" or args.precond != "mg":  # comparator line: no Vanka sweep in it
             line["sweep"] = line["roofline"] = None
         elif args.sweep != "fused":  # comparator line: the roofline accounting is the fused kernel's
             line["roofline"] = None
@@ -360,7 +364,11 @@ def main():
     ap.add_argument("--agglom", type=int, default=64)
     ap.add_argument("--relax", choices=["vanka", "bs", "su"], default="vanka",
                     help="V-cycle relaxation; bs / su are the paper's same-run comparators (configs[4], 1 GPU)")
+    ap.add_argument("--precond", choices=["mg", "bt"], default="mg",
+                    help="FGMRES preconditioner; bt = the paper's block-triangular comparator (configs[4], 1 GPU)")
     args = ap.parse_args()
+    if args.precond != "mg" and (args.gpus > 1 or args.impl == "reference"):
+        ap.error("--precond bt: single-GPU comparator runs of the svk arm only")
     if args.relax != "vanka" and (args.gpus > 1 or args.impl == "reference"):
         ap.error("--relax bs/su: single-GPU comparator runs of the svk arm only")
     if args.warmup < 3:

@@ -131,7 +131,21 @@ typedef struct svk_config {
   double relax_omega;    /* BS: omega_BS of alg:bs line 3-4 (unused by SU); default 1 */
   double jacobi_omega;   /* BS / SU: weight of the Jacobi iteration on S; default 0.8
                             (SU: 0.4, "optimal Jacobi weight") */
+  int32_t precond;       /* enum svk_precond: FGMRES preconditioner; default MG */
+  int32_t bt_cycles;     /* BLOCK_TRIANGULAR: V-cycles per block; default 3 */
+  int32_t bt_nu;         /* BLOCK_TRIANGULAR: Jacobi sweeps before / after; default 3 (V(3,3)) */
+  int32_t bt_reserved;
+  double bt_omega_u;     /* BLOCK_TRIANGULAR: Jacobi weight on L; default 1.0 */
+  double bt_omega_p;     /* BLOCK_TRIANGULAR: Jacobi weight on M; default 0.6 */
 } svk_config;
+
+/* FGMRES preconditioner:
+ * MG               -- one monolithic V(nu_pre, nu_post) cycle with svk_config.relax (alg:mg);
+ * BLOCK_TRIANGULAR -- alg:bt: [[L, B^T],[0, -M]] (du, dp) = r with M the Q1
+ *                     pressure mass matrix; M dp = -r_p, then L du = r_u - B^T dp, each by
+ *                     bt_cycles V(bt_nu, bt_nu) multigrid cycles with weighted Jacobi.
+ *                     Single-GPU comparator. */
+enum svk_precond { SVK_PRECOND_MG = 0, SVK_PRECOND_BLOCK_TRIANGULAR = 1 };
 
 /* Relaxation of the V-cycle (alg:mg "Relax on u_l and p_l"):
  * VANKA           -- additive Vanka (alg:vk), the hot path;
@@ -242,6 +256,12 @@ int svk_coarse_solve(svk_ctx* ctx, const double* b, double* x, void* stream);
  * Layout, ownership and stream semantics as svk_vanka_sweep; x_out must not alias
  * x_in or b.  SVK_ERR_INVALID on a bad level / pointer / aliasing. */
 int svk_relax_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, void* stream);
+
+/* z = M b on the finest level with the CONFIGURED FGMRES preconditioner
+ * (svk_config.precond): MG = one V-cycle from zero (as svk_vcycle with x = 0);
+ * BLOCK_TRIANGULAR = alg:bt.  b: residual-type vector (Dirichlet entries 0);
+ * z: output, fully overwritten, must not alias b.  Asynchronous on `stream`. */
+int svk_precond_apply(svk_ctx* ctx, const double* b, double* z, void* stream);
 
 /* One V(nu_pre, nu_post) cycle (alg:mg) on the finest level; x is
  * in/out (a preconditioner application passes x = 0).  b and x must not alias. */

@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(128) k_prolong_q1(LevelGeom gf, LevelGeom gc, 
 }
 
 // r_c = P^T r_f, coarse Dirichlet rows and padding set to 0
-__global__ void k_restrict(LevelGeom gf, LevelGeom gc, const double* __restrict__ rf, double* __restrict__ rc) {
-  const int plane = blockIdx.z;
+__global__ void k_restrict(LevelGeom gf, LevelGeom gc, const double* __restrict__ rf, double* __restrict__ rc,
+                           int plane0) {
+  const int plane = plane0 + blockIdx.z;  // planes plane0 .. plane0 + gridDim.z - 1
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (plane < 2) {

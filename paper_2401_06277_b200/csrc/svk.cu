@@ -22,6 +22,7 @@
 #include "sweep_fused.cuh"
 #include "residual_strip.cuh"
 #include "relax_bs.cuh"
+#include "bt.cuh"
 #include "dist.cuh"
 
 using namespace svk;
@@ -50,6 +51,11 @@ struct svk_ctx {
   // Braess-Sarazin / Schur-Uzawa comparators (relax_bs.cuh)
   double* d_schur = nullptr;                 // nlev * kSchurStride class stencils of S
   std::vector<double*> p_rhs, p_dp0, p_dp1;  // per level, pressure-plane sized
+  // block-triangular preconditioner (bt.cuh)
+  double* d_btb = nullptr;                   // finest-level right-hand side
+  double *d_bt_invL = nullptr, *d_bt_invM = nullptr;
+  int *d_bt_idxL = nullptr, *d_bt_idxM = nullptr;
+  int bt_niL = 0, bt_niM = 0;
   // Krylov
   std::vector<double*> V, Z;
   double* d_w = nullptr;
@@ -447,8 +453,92 @@ int op_relax(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
   return op_bs(ctx, l, xin, b, xout, x_zero, s);
 }
 
+// ---- block-triangular preconditioner (alg:bt) -------------------------------
+// plane range of a part: 0 = velocity planes [oux, op), 1 = pressure plane [op, len)
+void bt_range(const LevelGeom& g, int part, int64_t* off, int64_t* cnt) {
+  *off = part ? g.op : g.oux;
+  *cnt = part ? g.len - g.op : g.op - g.oux;
+}
+// scalar V(nu, nu) cycle with weighted Jacobi for block `part` on level l; x in/out
+int op_blk_mg(svk_ctx* ctx, int l, int part, const double* b, double* x, cudaStream_t s) {
+  const LevelGeom& g = ctx->g[l];
+  const svk_config& c = ctx->cfg;
+  int64_t off, cnt;
+  bt_range(g, part, &off, &cnt);
+  if (l == 0) {
+    CK(cudaMemsetAsync(x + off, 0, cnt * sizeof(double), s));
+    if (part == 0) k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_bt_invL, ctx->bt_niL, ctx->d_bt_idxL, b, x);
+    else k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_bt_invM, ctx->bt_niM, ctx->d_bt_idxM, b, x);
+    CKL();
+    ++ctx->launches;
+    return SVK_OK;
+  }
+  BtArgs a{};
+  a.g = g;
+  a.nu = c.nu;
+  a.part = part;
+  a.omega = part ? c.bt_omega_p : c.bt_omega_u;
+  const FusedFactors& F = ctx->h_fac[l];
+  for (int py = 0; py < 2; ++py)
+    for (int px = 0; px < 2; ++px) a.dinv[py][px] = 1.0 / F.L2D[py][px][2][2];
+  dim3 grid = plane_grid(g);
+  grid.z = part ? 1 : 2;
+  if (part) grid = dim3((unsigned)((g.pp + 31) / 32), (unsigned)((g.N + 1 + 7) / 8), 1);
+  auto smooth = [&]() -> int {
+    const double* src = x;
+    double* dst = ctx->ws_t[l];
+    for (int k = 0; k < c.bt_nu; ++k) {
+      k_bt_smooth<1><<<grid, kPlaneBlock, 0, s>>>(a, src, b, dst);
+      CKL();
+      ++ctx->launches;
+      double* nsrc = dst;
+      dst = const_cast<double*>(src);
+      src = nsrc;
+    }
+    if (src != x) CK(cudaMemcpyAsync(x + off, src + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return SVK_OK;
+  };
+  TRY(smooth());
+  k_bt_smooth<0><<<grid, kPlaneBlock, 0, s>>>(a, x, b, ctx->ws_r[l]);
+  CKL();
+  const LevelGeom& gc = ctx->g[l - 1];
+  dim3 cg = plane_grid(gc);
+  cg.z = part ? 1 : 2;
+  k_restrict<<<cg, kPlaneBlock, 0, s>>>(g, gc, ctx->ws_r[l], ctx->ws_b[l - 1], part ? 2 : 0);
+  CKL();
+  int64_t coff, ccnt;
+  bt_range(gc, part, &coff, &ccnt);
+  CK(cudaMemsetAsync(ctx->ws_x[l - 1] + coff, 0, ccnt * sizeof(double), s));
+  TRY(op_blk_mg(ctx, l - 1, part, ctx->ws_b[l - 1], ctx->ws_x[l - 1], s));
+  if (part == 0) {
+    const dim3 blk(32, 4), grd((unsigned)((gc.N + 31) / 32), (unsigned)((gc.N + 3) / 4), 2);
+    k_prolong_q2<<<grd, blk, 0, s>>>(g, gc, ctx->ws_x[l - 1], x, 0);
+  } else {
+    const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((gc.N + 1 + 3) / 4), 1);
+    k_prolong_q1<<<grd, blk, 0, s>>>(g, gc, ctx->ws_x[l - 1], x, 0);
+  }
+  CKL();
+  ctx->launches += 3;
+  TRY(smooth());
+  return SVK_OK;
+}
+// z = BT(r) on the finest level (alg:bt lines 1-2)
+int op_bt(svk_ctx* ctx, const double* r, double* z, cudaStream_t s) {
+  const int L = ctx->nlev - 1;
+  const LevelGeom& g = ctx->g[L];
+  k_bt_rhs<0><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, r, nullptr, ctx->d_btb);  // (0, 0, -r_p)
+  CKL();
+  CK(cudaMemsetAsync(z, 0, g.len * sizeof(double), s));
+  for (int k = 0; k < ctx->cfg.bt_cycles; ++k) TRY(op_blk_mg(ctx, L, 1, ctx->d_btb, z, s));  // M dp = -r_p
+  k_bt_rhs<1><<<plane_grid(g), kPlaneBlock, 0, s>>>(g, r, z, ctx->d_btb);  // (r_u - B^T dp, 0)
+  CKL();
+  for (int k = 0; k < ctx->cfg.bt_cycles; ++k) TRY(op_blk_mg(ctx, L, 0, ctx->d_btb, z, s));  // L du = ...
+  ctx->launches += 2;
+  return SVK_OK;
+}
+
 int op_restrict(svk_ctx* ctx, int l, const double* rf, double* rc, cudaStream_t s) {
-  k_restrict<<<plane_grid(ctx->g[l - 1]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], rf, rc);
+  k_restrict<<<plane_grid(ctx->g[l - 1]), kPlaneBlock, 0, s>>>(ctx->g[l], ctx->g[l - 1], rf, rc, 0);
   CKL();
   return SVK_OK;
 }
@@ -646,7 +736,8 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       const double* const* hV = (const double* const*)ctx->V.data();
       // z~_j = M V~_j : one V-cycle from zero
       CK(cudaEventRecord(ctx->ev[0], s));
-      TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
+      if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) TRY(op_bt(ctx, ctx->V[j], ctx->Z[j], s));
+      else TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
       CK(cudaEventRecord(ctx->ev[1], s));
       // w~ = A z~_j ; classical Gram-Schmidt pass against V~_0..V~_j (its dot
       // pass also yields |w~|^2) ; V~_j+1 = w~' with |w~'|
@@ -769,6 +860,11 @@ int free_ctx(svk_ctx* ctx) {
   for (BdTile* p : ctx->d_tiles) F(p);
   F(ctx->d_sw);
   F(ctx->d_schur);
+  F(ctx->d_btb);
+  F(ctx->d_bt_invL);
+  F(ctx->d_bt_invM);
+  F(ctx->d_bt_idxL);
+  F(ctx->d_bt_idxM);
   for (auto* v : {&ctx->p_rhs, &ctx->p_dp0, &ctx->p_dp1})
     for (double* p : *v) F(p);
   for (double* p : ctx->V) F(p);
@@ -926,6 +1022,27 @@ int create_impl(svk_ctx* ctx) {
     TRY(alloc_vec(ctx, &ctx->d_dbuf, (int64_t)kSlots * (gf.N + 1) * (gf.N + 1)));
   }
   CK(cudaMalloc(&ctx->d_part, (size_t)(kCgsMax + 1) * kDotBlocks * sizeof(double)));
+  if (c.precond == SVK_PRECOND_BLOCK_TRIANGULAR) {  // level-0 block inverses + finest rhs buffer
+    StencilConst t;
+    if (!build_tables(t, ctx->err)) return SVK_ERR_INVALID;
+    std::vector<double> iL, iM;
+    std::vector<int> xL, xM;
+    if (!build_bt_coarse(t, ctx->g[0], c.nu, iL, xL, iM, xM)) {
+      ctx->err = "block-triangular: singular level-0 block";
+      return SVK_ERR_SINGULAR;
+    }
+    ctx->bt_niL = (int)xL.size();
+    ctx->bt_niM = (int)xM.size();
+    CK(cudaMalloc(&ctx->d_bt_invL, iL.size() * sizeof(double)));
+    CK(cudaMalloc(&ctx->d_bt_invM, iM.size() * sizeof(double)));
+    CK(cudaMalloc(&ctx->d_bt_idxL, xL.size() * sizeof(int)));
+    CK(cudaMalloc(&ctx->d_bt_idxM, xM.size() * sizeof(int)));
+    CK(cudaMemcpy(ctx->d_bt_invL, iL.data(), iL.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bt_invM, iM.data(), iM.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bt_idxL, xL.data(), xL.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bt_idxM, xM.data(), xM.size() * sizeof(int), cudaMemcpyHostToDevice));
+    TRY(alloc_vec(ctx, &ctx->d_btb, ctx->g.back().len));
+  }
   if (c.relax != SVK_RELAX_VANKA) {  // comparator workspaces: S stencils + pressure-plane buffers
     StencilConst t;
     if (!build_tables(t, ctx->err)) return SVK_ERR_INVALID;
@@ -976,6 +1093,11 @@ int svk_config_default(svk_config* cfg, int32_t n_elem) {
   cfg->relax_omega = 1.0;
   cfg->jacobi_omega = 0.8;
   cfg->jacobi_sweeps = 3;
+  cfg->precond = SVK_PRECOND_MG;
+  cfg->bt_cycles = 3;
+  cfg->bt_nu = 3;
+  cfg->bt_omega_u = 1.0;
+  cfg->bt_omega_p = 0.6;
   return SVK_OK;
 }
 
@@ -996,6 +1118,9 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
   if (cfg->orth != SVK_ORTH_ADAPTIVE && cfg->orth != SVK_ORTH_CGS2) return SVK_ERR_INVALID;
   if (cfg->relax < SVK_RELAX_VANKA || cfg->relax > SVK_RELAX_SCHUR_UZAWA) return SVK_ERR_INVALID;
   if (cfg->sweep_impl < SVK_SWEEP_FUSED || cfg->sweep_impl > SVK_SWEEP_SIMPLE) return SVK_ERR_INVALID;
+  if (cfg->precond < SVK_PRECOND_MG || cfg->precond > SVK_PRECOND_BLOCK_TRIANGULAR) return SVK_ERR_INVALID;
+  if (cfg->precond == SVK_PRECOND_BLOCK_TRIANGULAR && (cfg->nranks > 1 || cfg->bt_cycles < 1 || cfg->bt_nu < 0))
+    return SVK_ERR_INVALID;  // single-GPU comparator
   if (cfg->relax != SVK_RELAX_VANKA && (cfg->nranks > 1 || !(cfg->relax_t > 0) || cfg->jacobi_sweeps < 0))
     return SVK_ERR_INVALID;  // the comparators are single-GPU
   if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
@@ -1119,6 +1244,21 @@ int svk_relax_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
   }
   if (ctx->cfg.relax == SVK_RELAX_VANKA) return svk_vanka_sweep(ctx, level, x_in, b, x_out, 1, stream);
   return op_bs(ctx, level, x_in, b, x_out, false, (cudaStream_t)stream);
+}
+
+int svk_precond_apply(svk_ctx* ctx, const double* b, double* z, void* stream) {
+  if (!ctx) return SVK_ERR_INVALID;
+  TRY(valid_ptr(ctx, b, "b"));
+  TRY(valid_ptr(ctx, z, "z"));
+  if (b == z) {
+    ctx->err = "z aliases b";
+    return SVK_ERR_INVALID;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int L = ctx->nlev - 1;
+  if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) return op_bt(ctx, b, z, s);
+  TRY(op_halo(ctx, L, const_cast<double*>(b), s));
+  return op_mg(ctx, L, b, z, true, s);
 }
 
 int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream) {

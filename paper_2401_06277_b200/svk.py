@@ -24,6 +24,7 @@ SWEEP = {"fused": 0, "unfused": 1, "simple": 2}
 ORTH = {"adaptive": 0, "cgs2": 1}
 TRANSPORT = {"none": 0, "nccl": 1, "emulated": 2}
 RELAX = {"vanka": 0, "bs": 1, "su": 2}
+PRECOND = {"mg": 0, "bt": 1}
 # comparator defaults: (t, omega_r, jacobi_omega, jacobi_sweeps)
 RELAX_DEFAULTS = {"bs": (1.0, 1.0, 0.8, 3), "su": (1.0, 1.0, 0.4, 1)}
 
@@ -38,7 +39,9 @@ class Config(C.Structure):
                 ("sweep_impl", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("transport", C.c_int32), ("agglom_rows", C.c_int32), ("emul_group", C.c_int32),
                 ("orth", C.c_int32), ("relax", C.c_int32), ("jacobi_sweeps", C.c_int32), ("nccl_id", C.c_uint8 * 128),
-                ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double)]
+                ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double),
+                ("precond", C.c_int32), ("bt_cycles", C.c_int32), ("bt_nu", C.c_int32), ("bt_reserved", C.c_int32),
+                ("bt_omega_u", C.c_double), ("bt_omega_p", C.c_double)]
 
 
 class LevelInfo(C.Structure):
@@ -71,6 +74,7 @@ EXPORTS = {
     "svk_matvec": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_vanka_sweep": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "svk_relax_sweep": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_precond_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_prolong_add": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_coarse_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -153,7 +157,8 @@ class Solver:
                  transport: str = "none", agglom_rows: int = 64, emul_group: int = 0, nccl_id: bytes | None = None,
                  orth: str = "adaptive", relax: str = "vanka", relax_t: float | None = None,
                  relax_omega: float | None = None, jacobi_omega: float | None = None,
-                 jacobi_sweeps: int | None = None):
+                 jacobi_sweeps: int | None = None, precond: str = "mg", bt_cycles: int = 3, bt_nu: int = 3,
+                 bt_omega_u: float = 1.0, bt_omega_p: float = 0.6):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
         "emulated" runs nranks logical ranks of one process on one device (one thread each).
@@ -172,6 +177,8 @@ class Solver:
         cfg.rank, cfg.nranks, cfg.transport = rank, nranks, TRANSPORT[transport]
         cfg.agglom_rows, cfg.emul_group, cfg.orth = agglom_rows, emul_group, ORTH[orth]
         cfg.relax = RELAX[relax]
+        cfg.precond, cfg.bt_cycles, cfg.bt_nu = PRECOND[precond], bt_cycles, bt_nu
+        cfg.bt_omega_u, cfg.bt_omega_p = bt_omega_u, bt_omega_p
         if relax != "vanka":
             d = RELAX_DEFAULTS[relax]
             cfg.relax_t = d[0] if relax_t is None else relax_t
@@ -290,6 +297,13 @@ class Solver:
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_relax_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
                                            self._vec(out, level, "x_out"), _stream(self.torch)))
+        return out
+
+    def precond_apply(self, b, out=None):
+        """z = M b with the configured FGMRES preconditioner (svk_precond_apply)."""
+        out = self.new_vector() if out is None else out
+        self._chk(self.lib.svk_precond_apply(self._h, self._vec(b, self.fine, "b"), self._vec(out, self.fine, "z"),
+                                             _stream(self.torch)))
         return out
 
     def restrict(self, level, rf, out=None):

@@ -105,3 +105,51 @@ def test_comparators_single_gpu_only(gpu):
     from paper_2401_06277_b200 import Solver, SvkError
     with pytest.raises(SvkError):
         Solver(64, rank=0, nranks=2, transport="emulated", relax="bs")
+
+
+# --------------------------------------------- block-triangular preconditioner (alg:bt)
+@pytest.mark.parametrize("N", [8, 16, 64, 256])
+def test_bt_precond_apply_parity(gpu, N):
+    from paper_2401_06277_b200 import Solver
+    O = oracle.Oracle(N)
+    O.set_precond(oracle.PRECOND_BT)
+    S = Solver(N, precond="bt")
+    for seed in (1, 2):
+        r = svk_inputs.random_vector(N, seed)
+        r[O.dirichlet(O.fine)] = 0.0
+        zo = O.precond_apply(r)
+        zg = to_np(S, S.precond_apply(S.from_compact(r)), S.fine)
+        assert rel(zg, zo) < 1e-12, (N, seed)
+
+
+def test_bt_parameters_parity(gpu):
+    from paper_2401_06277_b200 import Solver
+    O = oracle.Oracle(32)
+    O.set_precond(oracle.PRECOND_BT, cycles=2, nu=1, omega_u=0.7, omega_p=0.5)
+    S = Solver(32, precond="bt", bt_cycles=2, bt_nu=1, bt_omega_u=0.7, bt_omega_p=0.5)
+    r = svk_inputs.random_vector(32, 3)
+    r[O.dirichlet(O.fine)] = 0.0
+    assert rel(to_np(S, S.precond_apply(S.from_compact(r)), S.fine), O.precond_apply(r)) < 1e-12
+
+
+@pytest.mark.parametrize("N", [16, 64])
+def test_bt_fgmres_iterations(gpu, N):
+    from paper_2401_06277_b200 import Solver
+    O = oracle.Oracle(N)
+    O.set_precond(oracle.PRECOND_BT)
+    S = Solver(N, precond="bt")
+    bg, x0 = S.set_problem("mms_paper")
+    rep, _ = S.fgmres(bg, x0, rtol=1e-10, maxit=200)
+    bo, x0o = O.problem(oracle.MMS_PAPER)
+    _, its, _, _, st = O.fgmres(bo, x0o, rtol=1e-10, maxit=200)
+    assert st == 0 and rep["converged"] == 1
+    assert abs(rep["iterations"] - its) <= 1, (rep["iterations"], its)
+
+
+def test_precond_apply_mg_is_vcycle(gpu):
+    from paper_2401_06277_b200 import Solver
+    S = Solver(16)
+    O = oracle.Oracle(16)
+    r = svk_inputs.random_vector(16, 4)
+    r[O.dirichlet(O.fine)] = 0.0
+    assert rel(to_np(S, S.precond_apply(S.from_compact(r)), S.fine), O.vcycle(r)) < 1e-12

@@ -14,6 +14,12 @@ run 4096 bs 60
 run 1024 vanka 60
 run 1024 bs 60
 run 1024 su 200
+# block-triangular preconditioner (alg:bt)
+for n in 4096 1024; do
+  out=gpurun_out/compare_bt_${n}_$TAG.json
+  timeout 900 python bench.py --n $n --precond bt --maxit 60 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $out 2> ${out%.json}.err
+  python -c "import json;d=json.load(open('$out'));print('$n', 'bt', d['iterations'], round(d['time_to_solve_s'],4), 's', round(d['t_vcycle_s'],4), round(d['t_orth_s'],4), '%.2e'%d['rel_residual'])" || tail -3 ${out%.json}.err
+done
 # tuned (fused, 25 shared inverses) vs the paper's simple Vanka (per-patch inverses, unfused split)
 runs() {  # n sweep
   out=gpurun_out/compare_sweep_$2_$1_$TAG.json
