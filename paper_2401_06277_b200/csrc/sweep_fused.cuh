@@ -17,6 +17,7 @@
 #pragma once
 #include <cuda.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -783,6 +784,147 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   mbar_wait(&bars[(sE - sB) & 1], (phases >> ((sE - sB) & 1)) & 1u);
 }
 
+// -----------------------------------------------------------------------------
+// Pre-smoothing from zero (alg:mg line 2 on a V-cycle level entered with x = 0,
+// P:146): the residual IS b, and every generic patch window lies in the interior
+// (no Dirichlet point to mask), so this specialised kernel reads the patch
+// windows straight from a 4-pair b ring -- no residual phase, no residual ring,
+// no x loads: x_out = W sum_i V_i^T A_i^{-1} V_i b.  Same strip / warp layout and
+// owner-computes accumulation as k_vanka_fused; boundary patches from `bd`.
+// -----------------------------------------------------------------------------
+namespace fz0 {
+constexpr int BPR = 4, BPP = 4;  // b row pairs, b_p rows (slots = index & 3)
+constexpr int OBS = 0;
+constexpr int OBP = OBS + BPR * 4 * fz::W;
+constexpr int OMB = OBP + BPP * fz::PWID;
+constexpr int kSmemBytes = (OMB + 2) * 8;
+}  // namespace fz0
+__device__ __forceinline__ int z0_brow(int j, int c) {
+  return fz0::OBS + (((j - 1) >> 1) & 3) * 4 * fz::W + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
+}
+__device__ __forceinline__ int z0_bprow(int r) { return fz0::OBP + (r & 3) * fz::PWID; }
+
+__global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, const FusedFactors F,
+                                                            const __grid_constant__ FusedMaps M) {
+  extern __shared__ __align__(1024) double sm[];
+  const LevelGeom& g = A.g;
+  const int N = g.N, lat = g.lat;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int kx0 = blockIdx.x * fz::kNOUT;
+  const int y0 = g.r0 + blockIdx.y * A.chunk;
+  const int y1 = min(y0 + A.chunk, g.r1);
+  if (y0 >= y1) return;
+  const int xc0 = 2 * kx0 - 6;
+  const int sB = y0 - 1, sE = y1;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + fz0::OMB);
+  unsigned phases = 0u;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // data of step sB: b pairs sB-2 .. sB (rows 2sB-3 .. 2sB+2), b_p row sB -> barrier 0
+  if (t == 0) {
+    mbar_expect_tx(&bars[0], 3 * fz::kBBytes + fz::kBPBytes);
+    for (int p = sB - 2; p <= sB; ++p) tma_load_3d(sm + z0_brow(2 * p + 1, 0), &M.bv, xc0 + 2, 2 * p + 1, 0, &bars[0]);
+    tma_load_2d(sm + z0_bprow(sB), &M.bp, kx0 - 2, sB, &bars[0]);
+  }
+  const int pi = fz::kOWN * warp + lane;
+  const int kxp = kx0 - 1 + pi;
+  const bool owner = lane >= 1 && lane <= fz::kOWN;
+  double carry[3][2][2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) carry[r][c][0] = carry[r][c][1] = 0.0;
+  for (int s = sB; s <= sE; ++s) {
+    // step s: b pair s and b_p row s arrived on barrier (s-sB)&1.  After the CTA
+    // barrier every thread has finished step s-1 (windows of pairs s-3 .. s-1),
+    // so pair s+1 may replace the slot of pair s-3 and b_p row s+1 that of s-3.
+    const int bi = (s - sB) & 1;
+    mbar_wait(&bars[bi], (phases >> bi) & 1u);
+    phases ^= 1u << bi;
+    __syncthreads();
+    if (t == 0) {
+      uint64_t* nbar = &bars[bi ^ 1];
+      mbar_expect_tx(nbar, fz::kBBytes + fz::kBPBytes);
+      tma_load_3d(sm + z0_brow(2 * s + 3, 0), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
+      tma_load_2d(sm + z0_bprow(s + 1), &M.bp, kx0 - 2, s + 1, nbar);
+    }
+    double vx[25], vy[25];
+    double dp = 0.0;
+    const bool valid = kxp >= 0 && kxp <= N && s >= 0 && s <= N;
+    const bool generic = kxp >= 2 && kxp <= N - 2 && s >= 2 && s <= N - 2;
+    if (valid && generic) {  // window rows 2s-2 .. 2s+2, columns 2kxp-2 .. = b ring columns 2pi ..
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        const double* ru = sm + z0_brow(2 * s - 2 + oy, 0) + 2 * pi;
+        const double* rv = sm + z0_brow(2 * s - 2 + oy, 1) + 2 * pi;
+        const double2 u01 = lds2(ru), u23 = lds2(ru + 2), v01 = lds2(rv), v23 = lds2(rv + 2);
+        vx[oy * 5 + 0] = u01.x; vx[oy * 5 + 1] = u01.y; vx[oy * 5 + 2] = u23.x; vx[oy * 5 + 3] = u23.y;
+        vx[oy * 5 + 4] = ru[4];
+        vy[oy * 5 + 0] = v01.x; vy[oy * 5 + 1] = v01.y; vy[oy * 5 + 2] = v23.x; vy[oy * 5 + 3] = v23.y;
+        vy[oy * 5 + 4] = rv[4];
+      }
+      dp = solve_generic(vx, vy, sm[z0_bprow(s) + pi + 1], F);
+    } else if (valid) {
+      const int64_t nb = bd_count(N), bix = bd_index(kxp, s, N);
+#pragma unroll
+      for (int q = 0; q < 25; ++q) {
+        vx[q] = A.bd[q * nb + bix];
+        vy[q] = A.bd[(25 + q) * nb + bix];
+      }
+      dp = A.bd[50 * nb + bix];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 25; ++q) {
+        vx[q] = 0.0;
+        vy[q] = 0.0;
+      }
+    }
+    if (owner && s >= y0 && s < y1 && kxp < g.pp)
+      A.xout[g.op + (int64_t)s * g.pp + kxp] = kxp <= N ? A.omega * dp : 0.0;
+    const int ny = s - 1;
+    const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
+    const int i0 = 2 * kxp;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double* v = c ? vy : vx;
+      double S0[5], S1[5];
+#pragma unroll
+      for (int oy = 0; oy < 5; ++oy) {
+        const double r0 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 0], 1);
+        const double r1 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 1], 1);
+        const double l4 = __shfl_up_sync(0xffffffffu, v[oy * 5 + 4], 1);
+        S0[oy] = (oy < 3 ? carry[oy][c][0] : 0.0) + v[oy * 5 + 2] + l4 + r0;
+        S1[oy] = (oy < 3 ? carry[oy][c][1] : 0.0) + v[oy * 5 + 3] + r1;
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        carry[r][c][0] = S0[r + 2];
+        carry[r][c][1] = S1[r + 2];
+      }
+      if (rowout) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int j = 2 * ny + rr;
+          if (j > lat - 1) continue;
+          const bool jin = j >= 1 && j <= lat - 2;
+          const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
+          const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
+          const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
+          const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
+          *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
+              make_double2(in0 ? w0 * S0[rr] : 0.0, in1 ? w1 * S1[rr] : 0.0);
+        }
+      }
+    }
+  }
+  const int bl = (sE + 1 - sB) & 1;
+  mbar_wait(&bars[bl], (phases >> bl) & 1u);
+}
+
 inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const double* /*d_inv*/, double* d_fac,
                                int* d_status) {
   k_factor_setup<<<nlev, 256>>>(d_Ns, nu, d_fac, d_status);
@@ -851,7 +993,7 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_done[dev]) {
     cudaFuncSetAttribute(k_vanka_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmemBytes);
-    cudaFuncSetAttribute(k_vanka_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmemBytes);
+    cudaFuncSetAttribute(k_vanka_zero, cudaFuncAttributeMaxDynamicSharedMemorySize, fz0::kSmemBytes);
     attr_done[dev] = true;
   }
   const int ncover = (int)std::max<int64_t>(g.pu / 2, g.pp);
@@ -864,7 +1006,7 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   if (xin && (!make_vel_map(&M.xv, g, xin) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
   const dim3 grid(nstrips, (g.r1 - g.r0 + A.chunk - 1) / A.chunk);
   if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
-  else k_vanka_fused<true><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
+  else k_vanka_zero<<<grid, fz::kNT, fz0::kSmemBytes, s>>>(A, F, M);
   return 0;
 }
 
