@@ -18,11 +18,28 @@
 
 namespace svk {
 
+// Rings of the residual kernels: TMA data two steps ahead (three mbarriers), so
+// x keeps 6 row pairs (3 in use + 2 in flight), p 8 rows, b 4 pairs, b_p 4 rows.
 namespace rz {
-constexpr int ORS = fz::ORS;                  // MODE 1 exchange rows: [step parity][5][128]
-constexpr int OMB = ORS + 2 * 5 * fz::kNT;
-constexpr int kSmemBytes = (OMB + 2) * 8;
+constexpr int OXS = fz::OXS;                  // x pairs (6), as the sweep
+constexpr int OPS = fz::OPS;                  // p rows (8), as the sweep
+constexpr int OBS = OPS + 8 * fz::PXS;        // b pairs (4)
+constexpr int OBP = OBS + 4 * 4 * fz::W;      // b_p rows (4)
+constexpr int ORS = OBP + 4 * fz::PWID;       // MODE 1 exchange rows: [step parity][5][128]
+constexpr int OMB = ORS + 2 * 5 * fz::kNT;    // 3 mbarriers
+constexpr int kSmemBytes = (OMB + 4) * 8;
+static_assert((OBS * 8) % 128 == 0 && (OBP * 8) % 128 == 0, "TMA smem alignment");
+static_assert(2 * (kSmemBytes + 1024) <= 232448, "two CTAs per SM");
 }  // namespace rz
+__device__ __forceinline__ int rz_bpair(int p) { return rz::OBS + (p & 3) * 4 * fz::W; }
+struct RingRz {
+  static __device__ __forceinline__ int x(int j, int c) { return xrow(j, c); }
+  static __device__ __forceinline__ int p(int r) { return prow(r); }
+  static __device__ __forceinline__ int b(int j, int c) {
+    return rz_bpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
+  }
+  static __device__ __forceinline__ int bp(int r) { return rz::OBP + (r & 3) * fz::PWID; }
+};
 
 struct ResidArgs {
   LevelGeom g;   // fine level
@@ -59,40 +76,40 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // data of the first step: x pairs spB-1 .. spB+1, p rows spB .. spB+2, b pair spB, b_p row spB+1
-  if (t == 0) {
-    const unsigned bytes = 3 * fz::kXBytes + 3 * fz::kPBytes + (NOB ? 0u : fz::kBBytes + fz::kBPBytes);
-    mbar_expect_tx(&bars[0], bytes);
-    for (int p = spB - 1; p <= spB + 1; ++p) tma_load_3d(sm + xpair(p), &M.xv, xc0, 2 * p + 1, 0, &bars[0]);
-    for (int r = spB; r <= spB + 2; ++r) tma_load_2d(sm + prow(r), &M.xp, pc0, r, &bars[0]);
+  // data of step sp: x pairs up to sp+1, p rows up to sp+2, b pair sp, b_p row sp+1
+  auto issue = [&](int sp, uint64_t* bar, bool first) {
+    const unsigned nx = first ? 3 : 1;
+    mbar_expect_tx(bar, nx * (fz::kXBytes + fz::kPBytes) + (NOB ? 0u : fz::kBBytes + fz::kBPBytes));
+    for (int p = sp + 2 - (int)nx; p <= sp + 1; ++p) tma_load_3d(sm + xpair(p), &M.xv, xc0, 2 * p + 1, 0, bar);
+    for (int r = sp + 3 - (int)nx; r <= sp + 2; ++r) tma_load_2d(sm + prow(r), &M.xp, pc0, r, bar);
     if (!NOB) {
-      tma_load_3d(sm + bpair(spB), &M.bv, xc0 + 2, 2 * spB + 1, 0, &bars[0]);
-      tma_load_2d(sm + bprow(spB + 1), &M.bp, kx0 - 2, spB + 1, &bars[0]);
+      tma_load_3d(sm + rz_bpair(sp), &M.bv, xc0 + 2, 2 * sp + 1, 0, bar);
+      tma_load_2d(sm + RingRz::bp(sp + 1), &M.bp, kx0 - 2, sp + 1, bar);
     }
+  };
+  if (t == 0) {  // the first two steps
+    issue(spB, &bars[0], true);
+    issue(spB + 1, &bars[1], false);
   }
   double rc_carry[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // MODE 1: open coarse rows sp-1 .. sp+1
   double pc_carry[2] = {0.0, 0.0};                              // MODE 1: open coarse pressure rows
+  int slot = 0;                                                 // (sp - spB) % 3
   for (int sp = spB; sp <= spE; ++sp) {
-    const int k = sp - spB;
-    mbar_wait(&bars[k & 1], (phases >> (k & 1)) & 1u);
-    phases ^= 1u << (k & 1);
-    if (t == 0) {  // prefetch step sp+1: x pair sp+2, p row sp+3, b pair sp+1, b_p row sp+2
-      uint64_t* nb = &bars[(k + 1) & 1];
-      mbar_expect_tx(nb, fz::kXBytes + fz::kPBytes + (NOB ? 0u : fz::kBBytes + fz::kBPBytes));
-      tma_load_3d(sm + xpair(sp + 2), &M.xv, xc0, 2 * sp + 5, 0, nb);
-      tma_load_2d(sm + prow(sp + 3), &M.xp, pc0, sp + 3, nb);
-      if (!NOB) {
-        tma_load_3d(sm + bpair(sp + 1), &M.bv, xc0 + 2, 2 * sp + 3, 0, nb);
-        tma_load_2d(sm + bprow(sp + 2), &M.bp, kx0 - 2, sp + 2, nb);
-      }
-    }
+    mbar_wait(&bars[slot], (phases >> slot) & 1u);
+    phases ^= 1u << slot;
+    // prefetch step sp+2 (x pair sp+3 -> slot of sp-3, p row sp+4 -> slot of sp-4,
+    // b pair sp+2 -> slot of sp-2, b_p row sp+3 -> slot of sp-1): every thread has
+    // passed the barrier of step sp-1, i.e. finished the residual of step sp-1.
+    const int nslot = slot == 0 ? 2 : slot - 1;  // (sp + 2 - spB) % 3
+    if (t == 0) issue(sp + 2, &bars[nslot], false);
     if (MODE == 0) {
       // lattice rows 2sp+1, 2sp+2 and pressure row sp+1 straight from registers:
       // thread t in [2, 122) owns node column kx0-2+t (lattice columns 2kx, 2kx+1)
-      const ResVals V = fused_residual_vals<false, NOB>(sm, g, F, sp, kx0);
+      const ResVals V = fused_residual_vals<false, NOB, RingRz>(sm, g, F, sp, kx0);
       const int kx = kx0 - 2 + t, i0 = 2 * kx;
       if (t >= 2 && t < fz::kNOUT + 2) {
         const double sg = NOB ? -1.0 : 1.0;  // NOB: the values are -A x
@@ -118,7 +135,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
       // pressure column a/2.  1D P^T weights around fine 2C: C even: -1/8, 3/8,
       // 1, 3/8, -1/8 at offsets -3, -1, 0, 1, 3; C odd: 3/4, 1, 3/4 at -1, 0, 1;
       // pressure: 1/2, 1, 1/2 around fine node 2C'.
-      const ResVals V = fused_residual_vals<false, NOB>(sm, g, F, sp, kx0);
+      const ResVals V = fused_residual_vals<false, NOB, RingRz>(sm, g, F, sp, kx0);
       double* xb = sm + rz::ORS + (sp & 1) * 5 * fz::kNT;
       xb[0 * fz::kNT + t] = V.u[0][1];
       xb[1 * fz::kNT + t] = V.u[0][3];
@@ -168,8 +185,13 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
         }
       }
     }
+    slot = slot == 2 ? 0 : slot + 1;
   }
-  mbar_wait(&bars[(spE - spB + 1) & 1], (phases >> ((spE - spB + 1) & 1)) & 1u);
+  // the two last prefetches (steps spE+1, spE+2) must land before the shared memory is released
+  mbar_wait(&bars[slot], (phases >> slot) & 1u);
+  phases ^= 1u << slot;
+  slot = slot == 2 ? 0 : slot + 1;
+  mbar_wait(&bars[slot], (phases >> slot) & 1u);
 }
 
 // MODE 0: out = b - A x (NOB = false) or A x (NOB = true) on level g.

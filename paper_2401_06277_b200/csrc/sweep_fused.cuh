@@ -393,7 +393,14 @@ struct ResVals {
   double u[2][4];  // [comp][(j0,c0), (j0,c0+1), (j1,c0), (j1,c0+1)], 0 on Dirichlet / outside points
   double p;        // pressure residual at node (kx0-2+t, sp+1), 0 outside
 };
-template <bool XZERO, bool NOB = false>
+// ring layout of the sweep kernel (x 6 pairs, p 8 rows, b 2 pairs, b_p 2 rows)
+struct RingFz {
+  static __device__ __forceinline__ int x(int j, int c) { return xrow(j, c); }
+  static __device__ __forceinline__ int p(int r) { return prow(r); }
+  static __device__ __forceinline__ int b(int j, int c) { return brow(j, c); }
+  static __device__ __forceinline__ int bp(int r) { return bprow(r); }
+};
+template <bool XZERO, bool NOB = false, class RG = RingFz>
 __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const LevelGeom& g, const FusedFactors& F,
                                                        int sp, int kx0) {
   const int N = g.N, lat = g.lat, t = threadIdx.x;
@@ -411,8 +418,8 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
     double U[5][5], V[5][5];  // window rows 2sp..2sp+4, lattice columns c0-2..c0+2 (x columns 2t..2t+4)
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const double* xu = sm + xrow(2 * sp + r, 0) + 2 * t;
-      const double* xv = sm + xrow(2 * sp + r, 1) + 2 * t;
+      const double* xu = sm + RG::x(2 * sp + r, 0) + 2 * t;
+      const double* xv = sm + RG::x(2 * sp + r, 1) + 2 * t;
       const double2 u01 = lds2(xu), u23 = lds2(xu + 2), v01 = lds2(xv), v23 = lds2(xv + 2);
       U[r][0] = u01.x; U[r][1] = u01.y; U[r][2] = u23.x; U[r][3] = u23.y; U[r][4] = xu[4];
       V[r][0] = v01.x; V[r][1] = v01.y; V[r][2] = v23.x; V[r][3] = v23.y; V[r][4] = xv[4];
@@ -420,7 +427,7 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
     double Pm[3][3];  // p rows sp..sp+2, nodes kx0-3+t .. kx0-1+t (p ring column node - (kx0-4))
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      const double* pr = sm + prow(sp + r) + t + 1;
+      const double* pr = sm + RG::p(sp + r) + t + 1;
 #pragma unroll
       for (int q = 0; q < 3; ++q) Pm[r][q] = pr[q];
     }
@@ -497,14 +504,14 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
   ResVals R;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j0, comp) + 2 * t);
-    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + brow(j1, comp) + 2 * t);
+    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + RG::b(j0, comp) + 2 * t);
+    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + RG::b(j1, comp) + 2 * t);
     R.u[comp][0] = (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0;
     R.u[comp][1] = (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0;
     R.u[comp][2] = (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0;
     R.u[comp][3] = (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0;
   }
-  R.p = pok ? (NOB ? 0.0 : sm[bprow(nrow) + t]) - bu : 0.0;
+  R.p = pok ? (NOB ? 0.0 : sm[RG::bp(nrow) + t]) - bu : 0.0;
   return R;
 }
 // the same, stored into the residual rings (rows j0, j1 and pressure row sp+1)
