@@ -45,6 +45,9 @@ struct FusedFactors {
   double PBY[5][5];        // B_y: -h G row[oy] C^row[ox]
 };
 constexpr int kFacStride = (int)(sizeof(FusedFactors) / sizeof(double));
+}  // namespace svk
+#include "stencil_gen.cuh"
+namespace svk {
 
 // One CTA per level: build Lw, bx, by of the generic window, invert Lw, and
 // form the transformed blocks.  Output scaling folds the 1/2 of the inverse
@@ -144,6 +147,38 @@ __global__ void k_factor_setup(const int* __restrict__ Ns, double nu, double* __
       F->cpy[(ty - 3) * 3 + tx] = py;
     }
   }
+  __syncthreads();
+  // Enforce the identities the symmetry-shared solve (solve_gen.cuh) relies on,
+  // bitwise: B symmetric and invariant under the axis swap s(ty,tx) = (tx,ty)
+  // (Lw = nu(M (x) K + K (x) M) is), chy = s(chx), cpy = s(cpx) (b_y = s(b_x)).
+  // Each orbit is replaced by its mean (a change at the rounding level).
+  if (tid == 0) {
+    auto at = [&](int r, int c) -> double* {
+      const int ry = r / 5, rx = r % 5, cy_ = c / 5, cx_ = c % 5;
+      if (ry < 3 && rx < 3) return &F->bee[ry * 3 + rx][cy_ * 3 + cx_];
+      if (ry < 3) return &F->beo[ry * 2 + rx - 3][cy_ * 2 + cx_ - 3];
+      if (rx < 3) return &F->boe[(ry - 3) * 3 + rx][(cy_ - 3) * 3 + cx_];
+      return &F->boo[(ry - 3) * 2 + rx - 3][(cy_ - 3) * 2 + cx_ - 3];
+    };
+    auto sg = [](int r) { return (r % 5) * 5 + r / 5; };
+    for (int r = 0; r < 25; ++r)
+      for (int c = 0; c < 25; ++c) {
+        if ((r / 5 < 3) != (c / 5 < 3) || (r % 5 < 3) != (c % 5 < 3)) continue;
+        const int mr[4] = {r, c, sg(r), sg(c)}, mc[4] = {c, r, sg(c), sg(r)};
+        bool rep = true;
+        for (int m = 1; m < 4; ++m) rep = rep && (r * 25 + c <= mr[m] * 25 + mc[m]);
+        if (!rep) continue;
+        const double avg = ((*at(mr[0], mc[0]) + *at(mr[1], mc[1])) + (*at(mr[2], mc[2]) + *at(mr[3], mc[3]))) * 0.25;
+        for (int m = 0; m < 4; ++m) *at(mr[m], mc[m]) = avg;
+      }
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const double h2 = 0.5 * (F->chx[a * 2 + b] + F->chy[b * 3 + a]);
+        const double p2 = 0.5 * (F->cpx[a * 2 + b] + F->cpy[b * 3 + a]);
+        F->chx[a * 2 + b] = F->chy[b * 3 + a] = h2;
+        F->cpx[a * 2 + b] = F->cpy[b * 3 + a] = p2;
+      }
+  }
   for (int q = tid; q < 100; q += blockDim.x) {
     const int py = q / 50, px = (q / 25) % 2, b = (q / 5) % 5, a = q % 5;
     F->L2D[py][px][b][a] = nu * (c_st.MR[py][b] * c_st.KR[px][a] + c_st.KR[py][b] * c_st.MR[px][a]);
@@ -157,6 +192,26 @@ __global__ void k_factor_setup(const int* __restrict__ Ns, double nu, double* __
     const int oy = q / 5, ox = q % 5;
     F->PBX[oy][ox] = -h * c_st.CR[1][oy] * c_st.GR[1][ox];
     F->PBY[oy][ox] = -h * c_st.GR[1][oy] * c_st.CR[1][ox];
+  }
+  __syncthreads();
+  // Identities the shared-coefficient stencils (stencil_gen.cuh) rely on, made
+  // bitwise: L2D depends on (|db|, |da|) only (reflection-symmetric 1D Q2
+  // stencils) and L2D[py][px][b][a] = L2D[px][py][a][b]; PBY = PBX^T.
+  if (tid == 0) {
+    double L0[2][2][5][5];
+    for (int q = 0; q < 100; ++q) (&L0[0][0][0][0])[q] = (&F->L2D[0][0][0][0])[q];
+    for (int py = 0; py < 2; ++py)
+      for (int px = 0; px < 2; ++px)
+        for (int bi = 0; bi < 5; ++bi)
+          for (int ai = 0; ai < 5; ++ai) {
+            const int b = abs(bi - 2), a = abs(ai - 2);
+            int kp = py, kq = px, k1 = b, k2 = a;
+            if (py == 0 && px == 1) { kp = 1; kq = 0; k1 = a; k2 = b; }
+            else if (py == px) { k1 = min(a, b); k2 = max(a, b); }
+            F->L2D[py][px][bi][ai] = L0[kp][kq][k1 + 2][k2 + 2];
+          }
+    for (int oy = 0; oy < 5; ++oy)
+      for (int ox = 0; ox < 5; ++ox) F->PBY[oy][ox] = F->PBX[ox][oy];
   }
   if (tid == 0) {
     double s = 0;
@@ -431,51 +486,10 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
 #pragma unroll
       for (int q = 0; q < 3; ++q) Pm[r][q] = pr[q];
     }
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      if (r <= 2) {  // odd row j0 sees window rows 0..2 (b = r-1)
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-          const double c = F.L2D[1][0][r + 1][a];
-          ax[0] = fma(c, U[r][a], ax[0]);
-          ax[4] = fma(c, V[r][a], ax[4]);
-        }
-#pragma unroll
-        for (int a = 1; a < 4; ++a) {  // odd column (window column 3): taps 2..4
-          const double c = F.L2D[1][1][r + 1][a];
-          ax[1] = fma(c, U[r][a + 1], ax[1]);
-          ax[5] = fma(c, V[r][a + 1], ax[5]);
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < 5; ++a) {  // even row j1 sees window rows 0..4 (b = r-2)
-        const double c = F.L2D[0][0][r][a];
-        ax[2] = fma(c, U[r][a], ax[2]);
-        ax[6] = fma(c, V[r][a], ax[6]);
-      }
-#pragma unroll
-      for (int a = 1; a < 4; ++a) {
-        const double c = F.L2D[0][1][r][a];
-        ax[3] = fma(c, U[r][a + 1], ax[3]);
-        ax[7] = fma(c, V[r][a + 1], ax[7]);
-      }
-    }
+    stencil_L_sym(U, V, ax, F);  // shared-coefficient form (stencil_gen.cuh)
     const bool pint = na >= 1 && na <= N - 1 && nrow >= 1 && nrow <= N - 1;
     if (pint) {  // B u on the interior pressure-row pattern (window = U/V)
-#pragma unroll
-      for (int r = 1; r <= 3; ++r) {
-        bu = fma(F.PBX[r][0], U[r][0], bu);
-        bu = fma(F.PBX[r][1], U[r][1], bu);
-        bu = fma(F.PBX[r][3], U[r][3], bu);
-        bu = fma(F.PBX[r][4], U[r][4], bu);
-      }
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        if (r == 2) continue;
-        bu = fma(F.PBY[r][1], V[r][1], bu);
-        bu = fma(F.PBY[r][2], V[r][2], bu);
-        bu = fma(F.PBY[r][3], V[r][3], bu);
-      }
+      bu = stencil_B_sym(U, V, F);
     } else if (pok) {  // boundary pressure node: its B rows from the class table (B = -h PB)
       const int cls = (nrow == 0 ? 0 : (nrow == N ? 2 : 1)) * 3 + (na == 0 ? 0 : (na == N ? 2 : 1));
       const double* pbx = c_st.PB[0][cls];
@@ -562,62 +576,9 @@ __device__ __forceinline__ void inv_transform(double (&v)[25]) {
 #pragma unroll
   for (int r = 0; r < 5; ++r) SVK_UNSPLIT5(v, r * 5, 1);
 }
-// yhat = B rhat for both components at once: every coefficient is loaded once
-// and feeds two FMAs; all rows of a block accumulate in parallel (ILP).
-template <int NB>
-__device__ __forceinline__ void block_mv2(double (&vx)[25], double (&vy)[25], const double (&B)[NB][NB],
-                                          const int (&pos)[NB]) {
-  double sx[NB], sy[NB];
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    sx[r] = 0.0;
-    sy[r] = 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    const double ix = vx[pos[q]], iy = vy[pos[q]];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      const double c = B[r][q];
-      sx[r] = fma(c, ix, sx[r]);
-      sy[r] = fma(c, iy, sy[r]);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    vx[pos[r]] = sx[r];
-    vy[pos[r]] = sy[r];
-  }
-}
-
-// Generic patch: (vx, vy, rp) = patch residual in; (vx, vy) = (du, dv) out; returns dp.
-__device__ __forceinline__ double solve_generic(double (&vx)[25], double (&vy)[25], double rp, const FusedFactors& F) {
-  constexpr int pee[9] = {0, 1, 2, 5, 6, 7, 10, 11, 12};
-  constexpr int peo[6] = {3, 4, 8, 9, 13, 14};
-  constexpr int poe[6] = {15, 16, 17, 20, 21, 22};
-  constexpr int poo[4] = {18, 19, 23, 24};
-  fwd_transform(vx);
-  fwd_transform(vy);
-  double sx = 0.0, sy = 0.0;
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    sx = fma(F.chx[q], vx[peo[q]], sx);
-    sy = fma(F.chy[q], vy[poe[q]], sy);
-  }
-  const double dp = (sx + sy - rp) * F.inv_sigma;
-  block_mv2<9>(vx, vy, F.bee, pee);
-  block_mv2<6>(vx, vy, F.beo, peo);
-  block_mv2<6>(vx, vy, F.boe, poe);
-  block_mv2<4>(vx, vy, F.boo, poo);
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    vx[peo[q]] = fma(-F.cpx[q], dp, vx[peo[q]]);
-    vy[poe[q]] = fma(-F.cpy[q], dp, vy[poe[q]]);
-  }
-  inv_transform(vx);
-  inv_transform(vy);
-  return dp;
-}
+}  // namespace svk
+#include "solve_gen.cuh"
+namespace svk {
 
 template <bool XZERO>
 __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F,
@@ -725,7 +686,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
         vy[oy * 5 + 0] = v01.x; vy[oy * 5 + 1] = v01.y; vy[oy * 5 + 2] = v23.x; vy[oy * 5 + 3] = v23.y;
         vy[oy * 5 + 4] = rv[4];
       }
-      dp = solve_generic(vx, vy, sm[rprow(s) + pi + 1], F);
+      dp = solve_generic_sym(vx, vy, sm[rprow(s) + pi + 1], F);
     } else if (valid) {  // precomputed by k_boundary_patches
       const int64_t nb = bd_count(N), bi = bd_index(kxp, s, N);
 #pragma unroll
@@ -874,7 +835,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
         vy[oy * 5 + 0] = v01.x; vy[oy * 5 + 1] = v01.y; vy[oy * 5 + 2] = v23.x; vy[oy * 5 + 3] = v23.y;
         vy[oy * 5 + 4] = rv[4];
       }
-      dp = solve_generic(vx, vy, sm[z0_bprow(s) + pi + 1], F);
+      dp = solve_generic_sym(vx, vy, sm[z0_bprow(s) + pi + 1], F);
     } else if (valid) {
       const int64_t nb = bd_count(N), bix = bd_index(kxp, s, N);
 #pragma unroll
