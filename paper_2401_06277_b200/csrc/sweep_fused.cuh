@@ -455,9 +455,12 @@ struct RingFz {
   static __device__ __forceinline__ int b(int j, int c) { return brow(j, c); }
   static __device__ __forceinline__ int bp(int r) { return bprow(r); }
 };
-template <bool XZERO, bool NOB = false, class RG = RingFz>
+// MASK = false (the fused sweep): Dirichlet / boundary-pressure rows are not
+// masked -- generic patches, the only readers of these residuals, have windows
+// strictly inside the domain (2 <= kx, ky <= N-2), so those values are never used.
+template <bool XZERO, bool NOB = false, class RG = RingFz, bool MASK = true>
 __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const LevelGeom& g, const FusedFactors& F,
-                                                       int sp, int kx0) {
+                                                       int sp, int kx0, const RG& rg = RG{}) {
   const int N = g.N, lat = g.lat, t = threadIdx.x;
   const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
@@ -473,8 +476,8 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
     double U[5][5], V[5][5];  // window rows 2sp..2sp+4, lattice columns c0-2..c0+2 (x columns 2t..2t+4)
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const double* xu = sm + RG::x(2 * sp + r, 0) + 2 * t;
-      const double* xv = sm + RG::x(2 * sp + r, 1) + 2 * t;
+      const double* xu = sm + rg.x(2 * sp + r, 0) + 2 * t;
+      const double* xv = sm + rg.x(2 * sp + r, 1) + 2 * t;
       const double2 u01 = lds2(xu), u23 = lds2(xu + 2), v01 = lds2(xv), v23 = lds2(xv + 2);
       U[r][0] = u01.x; U[r][1] = u01.y; U[r][2] = u23.x; U[r][3] = u23.y; U[r][4] = xu[4];
       V[r][0] = v01.x; V[r][1] = v01.y; V[r][2] = v23.x; V[r][3] = v23.y; V[r][4] = xv[4];
@@ -482,15 +485,15 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
     double Pm[3][3];  // p rows sp..sp+2, nodes kx0-3+t .. kx0-1+t (p ring column node - (kx0-4))
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      const double* pr = sm + RG::p(sp + r) + t + 1;
+      const double* pr = sm + rg.p(sp + r) + t + 1;
 #pragma unroll
       for (int q = 0; q < 3; ++q) Pm[r][q] = pr[q];
     }
     stencil_L_sym(U, V, ax, F);  // shared-coefficient form (stencil_gen.cuh)
     const bool pint = na >= 1 && na <= N - 1 && nrow >= 1 && nrow <= N - 1;
-    if (pint) {  // B u on the interior pressure-row pattern (window = U/V)
+    if (pint || !MASK) {  // B u on the interior pressure-row pattern (window = U/V)
       bu = stencil_B_sym(U, V, F);
-    } else if (pok) {  // boundary pressure node: its B rows from the class table (B = -h PB)
+    } else if (MASK && pok) {  // boundary pressure node: its B rows from the class table (B = -h PB)
       const int cls = (nrow == 0 ? 0 : (nrow == N ? 2 : 1)) * 3 + (na == 0 ? 0 : (na == N ? 2 : 1));
       const double* pbx = c_st.PB[0][cls];
       const double* pby = c_st.PB[1][cls];
@@ -518,29 +521,76 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
   ResVals R;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + RG::b(j0, comp) + 2 * t);
-    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + RG::b(j1, comp) + 2 * t);
-    R.u[comp][0] = (j0ok && c0ok) ? b0.x - ax[4 * comp + 0] : 0.0;
-    R.u[comp][1] = (j0ok && c1ok) ? b0.y - ax[4 * comp + 1] : 0.0;
-    R.u[comp][2] = (j1ok && c0ok) ? b1.x - ax[4 * comp + 2] : 0.0;
-    R.u[comp][3] = (j1ok && c1ok) ? b1.y - ax[4 * comp + 3] : 0.0;
+    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + rg.b(j0, comp) + 2 * t);
+    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + rg.b(j1, comp) + 2 * t);
+    R.u[comp][0] = (!MASK || (j0ok && c0ok)) ? b0.x - ax[4 * comp + 0] : 0.0;
+    R.u[comp][1] = (!MASK || (j0ok && c1ok)) ? b0.y - ax[4 * comp + 1] : 0.0;
+    R.u[comp][2] = (!MASK || (j1ok && c0ok)) ? b1.x - ax[4 * comp + 2] : 0.0;
+    R.u[comp][3] = (!MASK || (j1ok && c1ok)) ? b1.y - ax[4 * comp + 3] : 0.0;
   }
-  R.p = pok ? (NOB ? 0.0 : sm[RG::bp(nrow) + t]) - bu : 0.0;
+  R.p = (!MASK || pok) ? (NOB ? 0.0 : sm[rg.bp(nrow) + t]) - bu : 0.0;
   return R;
 }
 // the same, stored into the residual rings (rows j0, j1 and pressure row sp+1)
+// Ring slots of one sweep step sp, maintained incrementally by the kernel (no
+// division by the non-power-of-two ring depths inside the step): xq = slot of x
+// pair sp-1, rq = residual-ring slot of lattice row 2sp-2.
+struct RingFzS {
+  int xq, rq;
+  __device__ __forceinline__ static RingFzS at(int sp) { return RingFzS{pmod(sp - 1, fz::XPR), pmod(2 * sp - 2, fz::RR)}; }
+  __device__ __forceinline__ void advance() {
+    xq = xq == fz::XPR - 1 ? 0 : xq + 1;
+    rq = rq + 2 >= fz::RR ? rq + 2 - fz::RR : rq + 2;
+  }
+  // x pair sp-1+d (d in -1..2)
+  __device__ __forceinline__ int xpair_d(int d) const {
+    int q = xq + d;
+    q = q >= fz::XPR ? q - fz::XPR : (q < 0 ? q + fz::XPR : q);
+    return fz::OXS + q * 4 * fz::W;
+  }
+  // lattice row j = 2sp+r (r in -3..4): pair sp + ((r-1)>>1) = sp-1 + d
+  __device__ __forceinline__ int xr(int r, int c) const { return xpair_d(((r - 1) >> 1) + 1) + c * 2 * fz::W + ((r - 1) & 1) * fz::W; }
+  // residual ring row 2sp-2+o (o in 0..6)
+  __device__ __forceinline__ int rr(int o, int c) const {
+    int q = rq + o;
+    q = q >= fz::RR ? q - fz::RR : q;
+    return fz::ORS + q * 2 * fz::W + c * fz::W;
+  }
+};
+// adapter for fused_residual_vals: rows addressed through the step's slots
+struct RingFzStep {
+  RingFzS S;
+  int sp;
+  __device__ __forceinline__ int x(int j, int c) const { return S.xr(j - 2 * sp, c); }
+  __device__ __forceinline__ int p(int r) const { return prow(r); }
+  __device__ __forceinline__ int b(int j, int c) const { return brow(j, c); }
+  __device__ __forceinline__ int bp(int r) const { return bprow(r); }
+};
 template <bool XZERO, bool NOB = false, int RRN = fz::RR, int ORSB = fz::ORS, int ORPB = fz::ORP>
 __device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
                                                int kx0) {
-  const ResVals R = fused_residual_vals<XZERO, NOB>(sm, g, F, sp, kx0);
-  const int t = threadIdx.x, j0 = 2 * sp + 1, j1 = 2 * sp + 2;
-  auto rr = [&](int j, int c) { return ORSB + pmod(j, RRN) * 2 * fz::W + c * fz::W; };
+  const RingFzStep rg{RingFzS::at(sp), sp};
+  const ResVals R = fused_residual_vals<XZERO, NOB, RingFzStep, false>(sm, g, F, sp, kx0, rg);
+  const int t = threadIdx.x;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    sts2(sm + rr(j0, comp) + 2 * t, R.u[comp][0], R.u[comp][1]);
-    sts2(sm + rr(j1, comp) + 2 * t, R.u[comp][2], R.u[comp][3]);
+    sts2(sm + rg.S.rr(3, comp) + 2 * t, R.u[comp][0], R.u[comp][1]);
+    sts2(sm + rg.S.rr(4, comp) + 2 * t, R.u[comp][2], R.u[comp][3]);
   }
   sm[ORPB + ((sp + 1) & 3) * fz::PWID + t] = R.p;
+}
+// the same with the step's slots supplied by the caller
+__device__ __forceinline__ void fused_residual_step(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
+                                                    int kx0, const RingFzS& S) {
+  const RingFzStep rg{S, sp};
+  const ResVals R = fused_residual_vals<false, false, RingFzStep, false>(sm, g, F, sp, kx0, rg);
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int comp = 0; comp < 2; ++comp) {
+    sts2(sm + S.rr(3, comp) + 2 * t, R.u[comp][0], R.u[comp][1]);
+    sts2(sm + S.rr(4, comp) + 2 * t, R.u[comp][2], R.u[comp][3]);
+  }
+  sm[fz::ORP + ((sp + 1) & 3) * fz::PWID + t] = R.p;
 }
 
 // forward even/odd transform of one 5-vector with stride st (in place)
@@ -642,6 +692,18 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 2; ++c) carry[r][c][0] = carry[r][c][1] = 0.0;
+  // per-thread output constants: column flags and multiplicity weights
+  // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
+  const int i0 = 2 * kxp;
+  const bool cin0 = i0 >= 1 && i0 <= lat - 2, cin1 = i0 + 1 <= lat - 2;
+  const bool cval0 = i0 <= lat - 1, cval1 = i0 + 1 <= lat - 1;
+  double wgt[2][2];  // [row parity][column parity]
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+      wgt[a][b] = A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0);
+  RingFzS S = RingFzS::at(sB);
   for (int s = sB; s <= sE; ++s) {
     // Data of step s (x pairs up to s+1, p rows up to s+2, b pair s, b_p row s+1)
     // arrived on barrier (s-sB+1)&1; prefetch step s+1 into the other one.
@@ -667,7 +729,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
       tma_load_3d(sm + bpair(s + 1), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
       tma_load_2d(sm + bprow(s + 2), &M.bp, kx0 - 2, s + 2, nbar);
     }
-    fused_residual<XZERO>(sm, A.g, F, s, kx0);
+    fused_residual_step(sm, A.g, F, s, kx0, S);
     __syncthreads();
 
     // ---- patch solve (alg:vk line 2: A_i delta_i = V_i r, exactly) ----
@@ -678,8 +740,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     if (valid && generic) {
 #pragma unroll
       for (int oy = 0; oy < 5; ++oy) {  // window columns 2kxp-2.. = ring columns 2pi .. 2pi+4
-        const double* ru = sm + rrow(2 * s - 2 + oy, 0) + 2 * pi;
-        const double* rv = sm + rrow(2 * s - 2 + oy, 1) + 2 * pi;
+        const double* ru = sm + S.rr(oy, 0) + 2 * pi;
+        const double* rv = sm + S.rr(oy, 1) + 2 * pi;
         const double2 u01 = lds2(ru), u23 = lds2(ru + 2), v01 = lds2(rv), v23 = lds2(rv + 2);
         vx[oy * 5 + 0] = u01.x; vx[oy * 5 + 1] = u01.y; vx[oy * 5 + 2] = u23.x; vx[oy * 5 + 3] = u23.y;
         vx[oy * 5 + 4] = ru[4];
@@ -711,7 +773,6 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     //      and x_out on rows 2s-2, 2s-1 (node row s-1), which are now complete ----
     const int ny = s - 1;
     const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
-    const int i0 = 2 * kxp;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const double* v = c ? vy : vx;
@@ -721,8 +782,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
         const double r0 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 0], 1);  // patch pi+1, window column 0
         const double r1 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 1], 1);  // patch pi+1, window column 1
         const double l4 = __shfl_up_sync(0xffffffffu, v[oy * 5 + 4], 1);    // patch pi-1, window column 4
-        S0[oy] = (oy < 3 ? carry[oy][c][0] : 0.0) + v[oy * 5 + 2] + l4 + r0;
-        S1[oy] = (oy < 3 ? carry[oy][c][1] : 0.0) + v[oy * 5 + 3] + r1;
+        S0[oy] = oy < 3 ? carry[oy][c][0] + v[oy * 5 + 2] + l4 + r0 : v[oy * 5 + 2] + l4 + r0;
+        S1[oy] = oy < 3 ? carry[oy][c][1] + v[oy * 5 + 3] + r1 : v[oy * 5 + 3] + r1;
       }
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
@@ -732,21 +793,23 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
       if (rowout) {
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-          const int j = 2 * ny + rr;
+          const int j = 2 * ny + rr;  // rr = row parity
           if (j > lat - 1) continue;
           const bool jin = j >= 1 && j <= lat - 2;
-          // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
-          const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
-          const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
-          const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
-          const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
-          const double2 x = XZERO ? make_double2(0.0, 0.0) : lds2(sm + xrow(j, c) + 2 * pi + 4);
-          const double o0 = in0 ? fma(w0, S0[rr], x.x) : (i0 <= lat - 1 ? x.x : 0.0);
-          const double o1 = in1 ? fma(w1, S1[rr], x.y) : (i0 + 1 <= lat - 1 ? x.y : 0.0);
+          const double2 x = lds2(sm + S.xr(rr - 2, c) + 2 * pi + 4);
+          double o0, o1;
+          if (jin && cin0 && cin1) {  // interior (all but the outermost rows / columns)
+            o0 = fma(wgt[rr][0], S0[rr], x.x);
+            o1 = fma(wgt[rr][1], S1[rr], x.y);
+          } else {
+            o0 = (jin && cin0) ? fma(wgt[rr][0], S0[rr], x.x) : (cval0 ? x.x : 0.0);
+            o1 = (jin && cin1) ? fma(wgt[rr][1], S1[rr], x.y) : (cval1 ? x.y : 0.0);
+          }
           *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) = make_double2(o0, o1);
         }
       }
     }
+    S.advance();
   }
   // the last prefetch (for step sE+1) must land before the CTA's shared memory is released
   mbar_wait(&bars[(sE - sB) & 1], (phases >> ((sE - sB) & 1)) & 1u);
@@ -806,6 +869,14 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 2; ++c) carry[r][c][0] = carry[r][c][1] = 0.0;
+  const int i0 = 2 * kxp;
+  const bool cin0 = i0 >= 1 && i0 <= lat - 2, cin1 = i0 + 1 <= lat - 2;
+  double wgt[2][2];  // [row parity][column parity], as in k_vanka_fused
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+      wgt[a][b] = A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0);
   for (int s = sB; s <= sE; ++s) {
     // step s: b pair s and b_p row s arrived on barrier (s-sB)&1.  After the CTA
     // barrier every thread has finished step s-1 (windows of pairs s-3 .. s-1),
@@ -855,7 +926,6 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
       A.xout[g.op + (int64_t)s * g.pp + kxp] = kxp <= N ? A.omega * dp : 0.0;
     const int ny = s - 1;
     const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
-    const int i0 = 2 * kxp;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const double* v = c ? vy : vx;
@@ -865,8 +935,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
         const double r0 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 0], 1);
         const double r1 = __shfl_down_sync(0xffffffffu, v[oy * 5 + 1], 1);
         const double l4 = __shfl_up_sync(0xffffffffu, v[oy * 5 + 4], 1);
-        S0[oy] = (oy < 3 ? carry[oy][c][0] : 0.0) + v[oy * 5 + 2] + l4 + r0;
-        S1[oy] = (oy < 3 ? carry[oy][c][1] : 0.0) + v[oy * 5 + 3] + r1;
+        S0[oy] = oy < 3 ? carry[oy][c][0] + v[oy * 5 + 2] + l4 + r0 : v[oy * 5 + 2] + l4 + r0;
+        S1[oy] = oy < 3 ? carry[oy][c][1] + v[oy * 5 + 3] + r1 : v[oy * 5 + 3] + r1;
       }
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
@@ -879,12 +949,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
           const int j = 2 * ny + rr;
           if (j > lat - 1) continue;
           const bool jin = j >= 1 && j <= lat - 2;
-          const double wy = A.scalar_w ? 1.0 : ((j & 1) ? 0.5 : (1.0 / 3.0));
-          const double w0 = A.omega * wy * (A.scalar_w ? 1.0 : 1.0 / 3.0);
-          const double w1 = A.omega * wy * (A.scalar_w ? 1.0 : 0.5);
-          const bool in0 = jin && i0 >= 1 && i0 <= lat - 2, in1 = jin && i0 + 1 <= lat - 2;
           *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
-              make_double2(in0 ? w0 * S0[rr] : 0.0, in1 ? w1 * S1[rr] : 0.0);
+              make_double2((jin && cin0) ? wgt[rr][0] * S0[rr] : 0.0, (jin && cin1) ? wgt[rr][1] * S1[rr] : 0.0);
         }
       }
     }
