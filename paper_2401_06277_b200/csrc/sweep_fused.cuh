@@ -969,7 +969,11 @@ inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const doubl
 inline int fused_chunk(const LevelGeom& g, int nstrips, int nsm) {
   const int rows = g.r1 - g.r0;
   const int resident = 2 * nsm;
-  const double work = (double)nstrips * rows / 128.0;
+  static const double target = [] {  // node rows per CTA the wave count aims at (SVK_CHUNK_ROWS: tuning aid)
+    const char* e = std::getenv("SVK_CHUNK_ROWS");
+    return e ? std::atof(e) : 64.0;
+  }();
+  const double work = (double)nstrips * rows / target;
   int waves = (int)(work / resident + 0.5);
   if (waves < 1) waves = 1;
   int chunks = (resident * waves) / nstrips;
