@@ -209,11 +209,8 @@ __device__ __forceinline__ int p2col(int c, int* f, double* w) {
 // points (4ex.., 4ey..) from its 3x3 coarse values -- 9 loads, 16 read-modify-
 // writes as double2.  Only the owned fine rows [2 r0, 2 r1) are written;
 // Dirichlet points (i or j = 0; 4 Nc is never produced) are left untouched.
-__global__ void __launch_bounds__(128) k_prolong_q2(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
-                                                    double* __restrict__ xf, int ey0) {
-  const int ex = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ey = ey0 + blockIdx.y * blockDim.y + threadIdx.y;
-  const int comp = blockIdx.z;
+__device__ __forceinline__ void prolong_q2_at(const LevelGeom& gf, const LevelGeom& gc, const double* __restrict__ ec,
+                                              double* __restrict__ xf, int ex, int ey, int comp) {
   if (ex >= gc.N || ey >= gc.N) return;
   const int jlo = max(2 * gf.r0, 1), jhi = min(2 * gf.r1, gf.lat - 1);
   const double* e = ec + (comp ? gc.ouy : gc.oux) + (int64_t)(2 * ey) * gc.pu + 2 * ex;
@@ -246,10 +243,8 @@ __global__ void __launch_bounds__(128) k_prolong_q2(LevelGeom gf, LevelGeom gc, 
 }
 // pressure (1D Q1: fine node 2a <- a, 2a+1 <- (a, a+1)/2): one thread per coarse
 // node (ax, ay) produces fine nodes (2ax, 2ax+1) x (2ay, 2ay+1); owned rows only.
-__global__ void __launch_bounds__(128) k_prolong_q1(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
-                                                    double* __restrict__ xf, int ay0) {
-  const int ax = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ay = ay0 + blockIdx.y * blockDim.y + threadIdx.y;
+__device__ __forceinline__ void prolong_q1_at(const LevelGeom& gf, const LevelGeom& gc, const double* __restrict__ ec,
+                                              double* __restrict__ xf, int ax, int ay) {
   if (ax > gc.N || ay > gc.N) return;
   const double* e = ec + gc.op + (int64_t)ay * gc.pp + ax;
   const bool rx = ax < gc.N, ry = ay < gc.N;  // neighbours exist
@@ -268,6 +263,19 @@ __global__ void __launch_bounds__(128) k_prolong_q1(LevelGeom gf, LevelGeom gc, 
     } else {
       f[0] += l;
     }
+  }
+}
+
+// One launch for both transfers: blockIdx.z = 0, 1 -> velocity components (coarse
+// element rows from ey0, ney of them), 2 -> pressure (coarse node rows from ay0, nay).
+__global__ void __launch_bounds__(128) k_prolong(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
+                                                 double* __restrict__ xf, int ey0, int ney, int ay0, int nay) {
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
+  if (blockIdx.z < 2) {
+    if (cy < ney) prolong_q2_at(gf, gc, ec, xf, cx, ey0 + cy, blockIdx.z);
+  } else if (cy < nay) {
+    prolong_q1_at(gf, gc, ec, xf, cx, ay0 + cy);
   }
 }
 
@@ -532,15 +540,18 @@ __global__ void k_coarse_invert(double* m, int n, int* perm, double* colk, int* 
   __syncthreads();
   if (!gj_invert(m, n, n, perm, colk, &flag) && threadIdx.x == 0) atomicExch(status, 1);
 }
-// x = pinv b on level 0: x zeroed by the caller, then scatter
+// x = pinv b on level 0: x zeroed by the caller, then scatter.  One warp per row
+// (coalesced row reads, fixed lane-strided partial sums + shuffle tree).
 __global__ void k_coarse_apply(const double* __restrict__ m, int ni, const int* __restrict__ idx,
                                const double* __restrict__ b, double* __restrict__ x) {
-  const int n = ni + 1;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < ni; ++c) s += m[(int64_t)r * n + c] * b[idx[c]];
-    x[idx[r]] = s;
-  }
+  const int n = ni + 1, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= ni) return;
+  double s = 0.0;
+  for (int c = lane; c < ni; c += 32) s = fma(m[(int64_t)r * n + c], b[idx[c]], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[idx[r]] = s;
 }
 
 // ---------------------------------------------------------------------------

@@ -467,8 +467,8 @@ int op_blk_mg(svk_ctx* ctx, int l, int part, const double* b, double* x, cudaStr
   bt_range(g, part, &off, &cnt);
   if (l == 0) {
     CK(cudaMemsetAsync(x + off, 0, cnt * sizeof(double), s));
-    if (part == 0) k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_bt_invL, ctx->bt_niL, ctx->d_bt_idxL, b, x);
-    else k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_bt_invM, ctx->bt_niM, ctx->d_bt_idxM, b, x);
+    if (part == 0) k_coarse_apply<<<(ctx->bt_niL + 3) / 4, 128, 0, s>>>(ctx->d_bt_invL, ctx->bt_niL, ctx->d_bt_idxL, b, x);
+    else k_coarse_apply<<<(ctx->bt_niM + 3) / 4, 128, 0, s>>>(ctx->d_bt_invM, ctx->bt_niM, ctx->d_bt_idxM, b, x);
     CKL();
     ++ctx->launches;
     return SVK_OK;
@@ -510,12 +510,9 @@ int op_blk_mg(svk_ctx* ctx, int l, int part, const double* b, double* x, cudaStr
   bt_range(gc, part, &coff, &ccnt);
   CK(cudaMemsetAsync(ctx->ws_x[l - 1] + coff, 0, ccnt * sizeof(double), s));
   TRY(op_blk_mg(ctx, l - 1, part, ctx->ws_b[l - 1], ctx->ws_x[l - 1], s));
-  if (part == 0) {
-    const dim3 blk(32, 4), grd((unsigned)((gc.N + 31) / 32), (unsigned)((gc.N + 3) / 4), 2);
-    k_prolong_q2<<<grd, blk, 0, s>>>(g, gc, ctx->ws_x[l - 1], x, 0);
-  } else {
-    const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((gc.N + 1 + 3) / 4), 1);
-    k_prolong_q1<<<grd, blk, 0, s>>>(g, gc, ctx->ws_x[l - 1], x, 0);
+  {  // velocity blocks (z = 0, 1) for part 0, pressure blocks (z = 2) for part 1
+    const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((gc.N + 1 + 3) / 4), part ? 3 : 2);
+    k_prolong<<<grd, blk, 0, s>>>(g, gc, ctx->ws_x[l - 1], x, 0, part ? 0 : gc.N, 0, part ? gc.N + 1 : 0);
   }
   CKL();
   ctx->launches += 3;
@@ -544,17 +541,13 @@ int op_restrict(svk_ctx* ctx, int l, const double* rf, double* rc, cudaStream_t 
 }
 int op_prolong_add(svk_ctx* ctx, int l, const double* ec, double* xf, cudaStream_t s) {
   const LevelGeom &gf = ctx->g[l], &gc = ctx->g[l - 1];
-  // velocity: coarse element rows covering the owned fine lattice rows [max(2 r0, 1), min(2 r1, lat - 1))
+  // velocity: coarse element rows covering the owned fine lattice rows [max(2 r0, 1), min(2 r1, lat - 1));
+  // pressure: coarse node rows covering the owned fine node rows; one launch for both
   const int jlo = std::max(2 * gf.r0, 1), jhi = std::min(2 * gf.r1, gf.lat - 1);
-  if (jhi > jlo) {
-    const int ey0 = jlo / 4, ney = (jhi - 1) / 4 - ey0 + 1;
-    const dim3 blk(32, 4), grd((unsigned)((gc.N + 31) / 32), (unsigned)((ney + 3) / 4), 2);
-    k_prolong_q2<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ey0);
-    CKL();
-  }
+  const int ey0 = jlo / 4, ney = jhi > jlo ? (jhi - 1) / 4 - ey0 + 1 : 0;
   const int ay0 = gf.r0 / 2, nay = (gf.r1 - 1) / 2 - ay0 + 1;
-  const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((nay + 3) / 4), 1);
-  k_prolong_q1<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ay0);
+  const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((std::max(ney, nay) + 3) / 4), 3);
+  k_prolong<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ey0, ney, ay0, nay);
   CKL();
   return SVK_OK;
 }
@@ -569,7 +562,7 @@ int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
     return SVK_OK;
   }
   CK(cudaMemsetAsync(x, 0, g.len * sizeof(double), s));
-  k_coarse_apply<<<1, 128, 0, s>>>(ctx->d_cmat, ctx->cni, ctx->d_cidx, b, x);
+  k_coarse_apply<<<(ctx->cni + 3) / 4, 128, 0, s>>>(ctx->d_cmat, ctx->cni, ctx->d_cidx, b, x);
   CKL();
   return SVK_OK;
 }
