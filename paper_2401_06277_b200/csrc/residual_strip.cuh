@@ -41,6 +41,16 @@ struct RingRz {
   static __device__ __forceinline__ int bp(int r) { return rz::OBP + (r & 3) * fz::PWID; }
 };
 
+// the same ring with the x-pair slots of step sp advanced incrementally (RingFzS)
+struct RingRzStep {
+  RingFzS S;
+  int sp;
+  __device__ __forceinline__ int x(int j, int c) const { return S.xr(j - 2 * sp, c); }
+  __device__ __forceinline__ int p(int r) const { return prow(r); }
+  __device__ __forceinline__ int b(int j, int c) const { return RingRz::b(j, c); }
+  __device__ __forceinline__ int bp(int r) const { return RingRz::bp(r); }
+};
+
 struct ResidArgs {
   LevelGeom g;   // fine level
   LevelGeom gc;  // coarse level (MODE 1)
@@ -98,7 +108,9 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   double rc_carry[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // MODE 1: open coarse rows sp-1 .. sp+1
   double pc_carry[2] = {0.0, 0.0};                              // MODE 1: open coarse pressure rows
   int slot = 0;                                                 // (sp - spB) % 3
+  RingFzS S = RingFzS::at(spB);
   for (int sp = spB; sp <= spE; ++sp) {
+    const RingRzStep rg{S, sp};
     mbar_wait(&bars[slot], (phases >> slot) & 1u);
     phases ^= 1u << slot;
     // prefetch step sp+2 (x pair sp+3 -> slot of sp-3, p row sp+4 -> slot of sp-4,
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
     if (MODE == 0) {
       // lattice rows 2sp+1, 2sp+2 and pressure row sp+1 straight from registers:
       // thread t in [2, 122) owns node column kx0-2+t (lattice columns 2kx, 2kx+1)
-      const ResVals V = fused_residual_vals<false, NOB, RingRz>(sm, g, F, sp, kx0);
+      const ResVals V = fused_residual_vals<false, NOB, RingRzStep>(sm, g, F, sp, kx0, rg);
       const int kx = kx0 - 2 + t, i0 = 2 * kx;
       if (t >= 2 && t < fz::kNOUT + 2) {
         const double sg = NOB ? -1.0 : 1.0;  // NOB: the values are -A x
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
       // pressure column a/2.  1D P^T weights around fine 2C: C even: -1/8, 3/8,
       // 1, 3/8, -1/8 at offsets -3, -1, 0, 1, 3; C odd: 3/4, 1, 3/4 at -1, 0, 1;
       // pressure: 1/2, 1, 1/2 around fine node 2C'.
-      const ResVals V = fused_residual_vals<false, NOB, RingRz>(sm, g, F, sp, kx0);
+      const ResVals V = fused_residual_vals<false, NOB, RingRzStep>(sm, g, F, sp, kx0, rg);
       double* xb = sm + rz::ORS + (sp & 1) * 5 * fz::kNT;
       xb[0 * fz::kNT + t] = V.u[0][1];
       xb[1 * fz::kNT + t] = V.u[0][3];
@@ -186,6 +198,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
       }
     }
     slot = slot == 2 ? 0 : slot + 1;
+    S.advance();
   }
   // the two last prefetches (steps spE+1, spE+2) must land before the shared memory is released
   mbar_wait(&bars[slot], (phases >> slot) & 1u);
