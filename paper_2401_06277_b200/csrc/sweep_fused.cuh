@@ -268,13 +268,21 @@ inline std::vector<BdTile> make_bd_tiles(int N) {
   return t;
 }
 
+// The tile's windows cover a band of 5 x (2n+3) lattice points (both components)
+// plus its n pressure nodes: the residual is evaluated once per band point
+// (phase 1), gathered into per-patch windows (phase 2), then the dense group
+// inverse is applied (phase 3).  Dirichlet / outside points carry 0 (they are
+// excluded from the patch unknowns, P:469 reading 7).
+constexpr int kBdBandW = 2 * kBdTile + 3;  // band length along the tile
 __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
                                                          const BdTile* __restrict__ tiles,
                                                          const double* __restrict__ x, const double* __restrict__ b,
                                                          double* __restrict__ bd) {
   constexpr int T = kBdTile, RS = 53;  // odd row stride: conflict-free 64-bit smem accesses
+  constexpr int NBAND = 2 * 5 * kBdBandW;
   __shared__ double Ai[kGroupStride];
   __shared__ double rv[T * RS];
+  __shared__ double band[NBAND + T];  // [comp][5 across][kBdBandW along] + pressure residuals
   const int N = g.N, lat = g.lat;
   const int64_t nb = bd_count(N);
   const BdTile tl = tiles[blockIdx.x];
@@ -282,23 +290,38 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
   if (max(tl.ky, ylo) < g.r0 - 1 || min(tl.ky, ylo) > g.r1) return;  // patch rows a slab uses: r0-1 .. r1
   const double* A = dinv + (size_t)tl.grp * kGroupStride;
   for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) Ai[q] = A[q];
+  // band origin: lattice point (2 kx - 2, 2 ky - 2) of the tile's first patch; "along" = tile direction
+  const int i0 = 2 * tl.kx - 2, j0 = 2 * tl.ky - 2;
+  const int nalong = 2 * tl.n + 3;
+  for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
+    double r = 0.0;
+    if (q < NBAND) {
+      const int comp = q / (5 * kBdBandW), rem = q % (5 * kBdBandW), ac = rem / kBdBandW, al = rem % kBdBandW;
+      const int i = i0 + (tl.dx ? al : ac), j = j0 + (tl.dx ? ac : al);
+      if (al < nalong && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
+        const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
+        double ax = 0.0;
+        if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
+        r = b[o] - ax;
+      }
+    } else if (q - NBAND < tl.n) {
+      const int pi = q - NBAND, kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
+      const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
+      r = b[p_at(g, kx, ky)] - ax;
+    }
+    band[q] = r;
+  }
+  __syncthreads();
   for (int q = threadIdx.x; q < T * kSlots; q += blockDim.x) {
-    const int pi = q % T, s = q / T;  // consecutive threads -> consecutive patches
+    const int pi = q % T, s = q / T;
     double r = 0.0;
     if (pi < tl.n) {
-      const int kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
-      if (s < 50) {
+      if (s < 50) {  // window (oy, ox) of patch pi: band across = oy (row tile) / ox, along = 2 pi + ox / oy
         const int comp = s / 25, oy = (s % 25) / 5, ox = s % 5;
-        const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
-        if (i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
-          const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-          double ax = 0.0;
-          if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
-          r = b[o] - ax;
-        }
+        const int ac = tl.dx ? oy : ox, al = 2 * pi + (tl.dx ? ox : oy);
+        r = band[comp * 5 * kBdBandW + ac * kBdBandW + al];
       } else {
-        const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
-        r = b[p_at(g, kx, ky)] - ax;
+        r = band[NBAND + pi];
       }
     }
     rv[pi * RS + s] = r;
