@@ -6,6 +6,35 @@
 
 namespace svk {
 
+// Programmatic dependent launch: the V-cycle kernels are launched with
+// programmaticStreamSerialization, so a kernel's CTAs are scheduled (and run their
+// dependency-free prologue) while the previous kernel drains; every such kernel
+// calls pdl_wait() before touching memory the previous kernel writes.  No kernel
+// triggers early, so the wait returns only when the previous grid has completed
+// and its writes are visible.  SVK_PDL=0 launches them plainly (wait is a no-op).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SVK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 constexpr int kSlots = 51;             // padded patch slots: 2 x 5x5 velocity window + 1 pressure
 constexpr int kGroupStride = kSlots * kSlots;
 
@@ -270,6 +299,7 @@ __device__ __forceinline__ void prolong_q1_at(const LevelGeom& gf, const LevelGe
 // element rows from ey0, ney of them), 2 -> pressure (coarse node rows from ay0, nay).
 __global__ void __launch_bounds__(128) k_prolong(LevelGeom gf, LevelGeom gc, const double* __restrict__ ec,
                                                  double* __restrict__ xf, int ey0, int ney, int ay0, int nay) {
+  pdl_wait();
   const int cx = blockIdx.x * blockDim.x + threadIdx.x;
   const int cy = blockIdx.y * blockDim.y + threadIdx.y;
   if (blockIdx.z < 2) {
@@ -544,6 +574,7 @@ __global__ void k_coarse_invert(double* m, int n, int* perm, double* colk, int* 
 // (coalesced row reads, fixed lane-strided partial sums + shuffle tree).
 __global__ void k_coarse_apply(const double* __restrict__ m, int ni, const int* __restrict__ idx,
                                const double* __restrict__ b, double* __restrict__ x) {
+  pdl_wait();
   const int n = ni + 1, lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= ni) return;

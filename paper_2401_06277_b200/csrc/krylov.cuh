@@ -12,6 +12,7 @@ constexpr int kRedThreads = 256;
 // out[m] (+)= sum_b partial[m*nb + b], one block per m, fixed order
 __global__ void k_reduce_partials(const double* __restrict__ partial, int nb, double* __restrict__ out, int accumulate) {
   __shared__ double sm[kRedThreads];
+  pdl_wait();
   const int m = blockIdx.x;
   double s = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s += partial[m * nb + b];
@@ -84,6 +85,7 @@ __device__ __forceinline__ void block_reduce_store_n(const double (&acc)[MM], in
 template <int MM>
 __global__ void __launch_bounds__(kRedThreads) k_cgs_dots(const VecList V, int m, const double* __restrict__ w,
                                                           const Seg3 S, double* __restrict__ partial) {
+  pdl_wait();
   double acc[MM];
 #pragma unroll
   for (int i = 0; i < MM; ++i) acc[i] = 0.0;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_dots(const VecList V, int m
 __global__ void __launch_bounds__(kRedThreads) k_cgs_update(const VecList V, int m, const double* __restrict__ c,
                                                             const double* __restrict__ w, double* __restrict__ wout,
                                                             const Seg3 S, double* __restrict__ partial) {
+  pdl_wait();
   const int64_t n2 = S.cum2[3];
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* o2 = reinterpret_cast<double2*>(wout);
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_update(const VecList V, int
 // c[i] = raw[i] * scale[i]  (device), for i < m
 __global__ void k_scale_coef(const double* __restrict__ raw, const double* __restrict__ scale, double* __restrict__ c,
                              int m) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) c[i] = raw[i] * scale[i];
 }

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
   // data of step sp: x pairs up to sp+1, p rows up to sp+2, b pair sp, b_p row sp+1
   auto issue = [&](int sp, uint64_t* bar, bool first) {
     const unsigned nx = first ? 3 : 1;
@@ -230,8 +231,8 @@ inline int launch_residual_strip(const LevelGeom& g, const LevelGeom* gc, const 
   if (!gc) {
     R.chunk = fused_chunk(g, nstrips, nsm);
     const dim3 grid(nstrips, (g.r1 - g.r0 + R.chunk - 1) / R.chunk);
-    if (b) k_residual_strip<false, 0><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
-    else k_residual_strip<true, 0><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
+    if (b) launch_pdl(k_residual_strip<false, 0>, grid, dim3(fz::kNT), rz::kSmemBytes, s, R, F, M);
+    else launch_pdl(k_residual_strip<true, 0>, grid, dim3(fz::kNT), rz::kSmemBytes, s, R, F, M);
   } else {
     if (!b) return -1;
     // coarse strips must cover the coarse pitch too: strip k owns coarse lattice columns [120k, 120k+120)
@@ -239,7 +240,7 @@ inline int launch_residual_strip(const LevelGeom& g, const LevelGeom* gc, const 
     const int ns = (ncov + fz::kNOUT - 1) / fz::kNOUT;
     R.chunk = std::max(1, fused_chunk(*gc, ns, nsm) / 2 + 1);
     const dim3 grid(ns, (gc->r1 - gc->r0 + R.chunk - 1) / R.chunk);
-    k_residual_strip<false, 1><<<grid, fz::kNT, rz::kSmemBytes, s>>>(R, F, M);
+    launch_pdl(k_residual_strip<false, 1>, grid, dim3(fz::kNT), rz::kSmemBytes, s, R, F, M);
   }
   return 0;
 }

@@ -547,7 +547,7 @@ int op_prolong_add(svk_ctx* ctx, int l, const double* ec, double* xf, cudaStream
   const int ey0 = jlo / 4, ney = jhi > jlo ? (jhi - 1) / 4 - ey0 + 1 : 0;
   const int ay0 = gf.r0 / 2, nay = (gf.r1 - 1) / 2 - ay0 + 1;
   const dim3 blk(32, 4), grd((unsigned)((gc.N + 1 + 31) / 32), (unsigned)((std::max(ney, nay) + 3) / 4), 3);
-  k_prolong<<<grd, blk, 0, s>>>(gf, gc, ec, xf, ey0, ney, ay0, nay);
+  launch_pdl(k_prolong, grd, blk, 0, s, gf, gc, ec, xf, ey0, ney, ay0, nay);
   CKL();
   return SVK_OK;
 }
@@ -562,7 +562,8 @@ int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
     return SVK_OK;
   }
   CK(cudaMemsetAsync(x, 0, g.len * sizeof(double), s));
-  k_coarse_apply<<<(ctx->cni + 3) / 4, 128, 0, s>>>(ctx->d_cmat, ctx->cni, ctx->d_cidx, b, x);
+  launch_pdl(k_coarse_apply, dim3((ctx->cni + 3) / 4), dim3(128), 0, s, (const double*)ctx->d_cmat, ctx->cni,
+             (const int*)ctx->d_cidx, b, x);
   CKL();
   return SVK_OK;
 }
@@ -629,11 +630,11 @@ int cgs_dots(svk_ctx* ctx, const double* const* dV, int m, const double* w, cons
   constexpr int kDot = 16;
   for (int c0 = 0; c0 < m; c0 += kDot) {
     const int mm = std::min(kDot, m - c0);
-    if (mm <= 4) k_cgs_dots<4><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
-    else if (mm <= 8) k_cgs_dots<8><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
-    else k_cgs_dots<16><<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, w, S, ctx->d_part);
+    if (mm <= 4) launch_pdl(k_cgs_dots<4>, dim3(kDotBlocks), dim3(kRedThreads), 0, s, veclist(dV + c0, mm), mm, w, S, ctx->d_part);
+    else if (mm <= 8) launch_pdl(k_cgs_dots<8>, dim3(kDotBlocks), dim3(kRedThreads), 0, s, veclist(dV + c0, mm), mm, w, S, ctx->d_part);
+    else launch_pdl(k_cgs_dots<16>, dim3(kDotBlocks), dim3(kRedThreads), 0, s, veclist(dV + c0, mm), mm, w, S, ctx->d_part);
     CKL();
-    k_reduce_partials<<<mm, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + off + c0, 0);
+    launch_pdl(k_reduce_partials, dim3(mm), dim3(kRedThreads), 0, s, (const double*)ctx->d_part, kDotBlocks, ctx->d_coef + off + c0, 0);
     CKL();
   }
   if (ctx->tr) TRY(op_allreduce(ctx, ctx->d_coef + off, m, s));
@@ -646,13 +647,13 @@ int cgs_update(svk_ctx* ctx, const double* const* dV, int m, int coff, const dou
   if (m == 0 && w != wout) CK(cudaMemcpyAsync(wout, w, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   for (int c0 = 0; c0 < m; c0 += kCgsMax) {
     const int mm = std::min(kCgsMax, m - c0);
-    k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist(dV + c0, mm), mm, ctx->d_coef + coff + c0, src, wout, S,
-                                                     ctx->d_part);
+    launch_pdl(k_cgs_update, dim3(kDotBlocks), dim3(kRedThreads), 0, s, veclist(dV + c0, mm), mm,
+               (const double*)(ctx->d_coef + coff + c0), src, wout, S, ctx->d_part);
     CKL();
     src = wout;
   }
   if (noff >= 0) {
-    k_reduce_partials<<<1, kRedThreads, 0, s>>>(ctx->d_part, kDotBlocks, ctx->d_coef + noff, 0);
+    launch_pdl(k_reduce_partials, dim3(1), dim3(kRedThreads), 0, s, (const double*)ctx->d_part, kDotBlocks, ctx->d_coef + noff, 0);
     CKL();
     if (ctx->tr) TRY(op_allreduce(ctx, ctx->d_coef + noff, 1, s));
   }
@@ -738,7 +739,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       dlist.assign(hV, hV + m);
       dlist.push_back(ctx->d_w);
       TRY(cgs_dots(ctx, dlist.data(), m + 1, ctx->d_w, S, oraw, s));
-      k_scale_coef<<<(m + 63) / 64, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o1, m);
+      launch_pdl(k_scale_coef, dim3((m + 63) / 64), dim3(64), 0, s, (const double*)(ctx->d_coef + oraw), (const double*)(ctx->d_coef + oinv), ctx->d_coef + o1, m);
       CKL();
       TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
@@ -754,7 +755,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       if (ctx->cfg.orth == SVK_ORTH_CGS2 || !(wp2 * kReorthKappa * kReorthKappa >= wn2)) {
         CK(cudaEventRecord(ctx->ev[3], s));
         TRY(cgs_dots(ctx, hV, m, ctx->V[j + 1], S, oraw, s));
-        k_scale_coef<<<(m + 63) / 64, 64, 0, s>>>(ctx->d_coef + oraw, ctx->d_coef + oinv, ctx->d_coef + o2, m);
+        launch_pdl(k_scale_coef, dim3((m + 63) / 64), dim3(64), 0, s, (const double*)(ctx->d_coef + oraw), (const double*)(ctx->d_coef + oinv), ctx->d_coef + o2, m);
         CKL();
         TRY(cgs_update(ctx, hV, m, o2, ctx->V[j + 1], ctx->V[j + 1], n, S, onrm, s));
         CK(cudaEventRecord(ctx->ev[4], s));

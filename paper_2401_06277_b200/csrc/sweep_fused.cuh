@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
   __shared__ double Ai[kGroupStride];
   __shared__ double rv[T * RS];
   __shared__ double band[NBAND + T];  // [comp][5 across][kBdBandW along] + pressure residuals
+  pdl_wait();
   const int N = g.N, lat = g.lat;
   const int64_t nb = bd_count(N);
   const BdTile tl = tiles[blockIdx.x];
@@ -675,6 +676,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, c
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
   // prologue: x pairs sB-3 .. sB+1 (rows 2sB-5 .. 2sB+4), p rows sB-2 .. sB+1,
   // b pairs sB-2, sB-1 (rows 2sB-3 .. 2sB), b_p rows sB-1, sB  -> barrier 0
   if (t == 0) {
@@ -878,6 +880,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, co
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
   // data of step sB: b pairs sB-2 .. sB (rows 2sB-3 .. 2sB+2), b_p row sB -> barrier 0
   if (t == 0) {
     mbar_expect_tx(&bars[0], 3 * fz::kBBytes + fz::kBPBytes);
@@ -1048,7 +1051,7 @@ inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsi
 inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,
                               const double* dinv, const BdTile* tiles, int ntiles, double* bd, const double* xin,
                               const double* b, double* xout, int nsm, cudaStream_t s) {
-  k_boundary_patches<<<(unsigned)ntiles, kBdThreads, 0, s>>>(g, nu, dinv, tiles, xin, b, bd);
+  launch_pdl(k_boundary_patches, dim3((unsigned)ntiles), dim3(kBdThreads), 0, s, g, nu, dinv, tiles, xin, b, bd);
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1066,8 +1069,8 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   if (!make_vel_map(&M.bv, g, b) || !make_p_map(&M.bp, g, b, fz::PWID)) return -2;
   if (xin && (!make_vel_map(&M.xv, g, xin) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
   const dim3 grid(nstrips, (g.r1 - g.r0 + A.chunk - 1) / A.chunk);
-  if (xin) k_vanka_fused<false><<<grid, fz::kNT, fz::kSmemBytes, s>>>(A, F, M);
-  else k_vanka_zero<<<grid, fz::kNT, fz0::kSmemBytes, s>>>(A, F, M);
+  if (xin) launch_pdl(k_vanka_fused<false>, grid, dim3(fz::kNT), fz::kSmemBytes, s, A, F, M);
+  else launch_pdl(k_vanka_zero, grid, dim3(fz::kNT), fz0::kSmemBytes, s, A, F, M);
   return 0;
 }
 
