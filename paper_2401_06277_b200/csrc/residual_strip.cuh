@@ -21,20 +21,25 @@ namespace svk {
 // Rings of the residual kernels: TMA data two steps ahead (three mbarriers), so
 // x keeps 6 row pairs (3 in use + 2 in flight), p 8 rows, b 4 pairs, b_p 4 rows.
 namespace rz {
-constexpr int OXS = fz::OXS;                  // x pairs (6), as the sweep
-constexpr int OPS = fz::OPS;                  // p rows (8), as the sweep
+constexpr int XPR = 6;                        // x pairs (width fz::WX)
+constexpr int OXS = 0;
+constexpr int OPS = OXS + XPR * 4 * fz::WX;   // p rows (8), as the sweep
 constexpr int OBS = OPS + 8 * fz::PXS;        // b pairs (4)
 constexpr int OBP = OBS + 4 * 4 * fz::W;      // b_p rows (4)
 constexpr int ORS = OBP + 4 * fz::PWID;       // MODE 1 exchange rows: [step parity][5][128]
 constexpr int OMB = ORS + 2 * 5 * fz::kNT;    // 3 mbarriers
 constexpr int kSmemBytes = (OMB + 4) * 8;
 static_assert((OBS * 8) % 128 == 0 && (OBP * 8) % 128 == 0, "TMA smem alignment");
-static_assert(2 * (kSmemBytes + 1024) <= 232448, "two CTAs per SM");
+static_assert(fz::kMinB * (kSmemBytes + 1024) <= 232448, "kMinB CTAs per SM");
 }  // namespace rz
 __device__ __forceinline__ int rz_bpair(int p) { return rz::OBS + (p & 3) * 4 * fz::W; }
+__device__ __forceinline__ int rz_prow(int r) { return rz::OPS + (r & 7) * fz::PXS; }
+__device__ __forceinline__ int rz_xpair(int p) { return rz::OXS + pmod(p, rz::XPR) * 4 * fz::WX; }
 struct RingRz {
-  static __device__ __forceinline__ int x(int j, int c) { return xrow(j, c); }
-  static __device__ __forceinline__ int p(int r) { return prow(r); }
+  static __device__ __forceinline__ int x(int j, int c) {
+    return rz_xpair((j - 1) >> 1) + c * 2 * fz::WX + ((j - 1) & 1) * fz::WX;
+  }
+  static __device__ __forceinline__ int p(int r) { return rz_prow(r); }
   static __device__ __forceinline__ int b(int j, int c) {
     return rz_bpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
   }
@@ -43,10 +48,10 @@ struct RingRz {
 
 // the same ring with the x-pair slots of step sp advanced incrementally (RingFzS)
 struct RingRzStep {
-  RingFzS S;
+  RingSlots<rz::XPR, rz::OXS> S;
   int sp;
   __device__ __forceinline__ int x(int j, int c) const { return S.xr(j - 2 * sp, c); }
-  __device__ __forceinline__ int p(int r) const { return prow(r); }
+  __device__ __forceinline__ int p(int r) const { return rz_prow(r); }
   __device__ __forceinline__ int b(int j, int c) const { return RingRz::b(j, c); }
   __device__ __forceinline__ int bp(int r) const { return RingRz::bp(r); }
 };
@@ -59,7 +64,7 @@ struct ResidArgs {
 };
 
 template <bool NOB, int MODE>
-__global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R, const FusedFactors F,
+__global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const ResidArgs R, const FusedFactors F,
                                                                const __grid_constant__ FusedMaps M) {
   extern __shared__ __align__(1024) double sm[];
   const LevelGeom& g = R.g;
@@ -95,8 +100,8 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   auto issue = [&](int sp, uint64_t* bar, bool first) {
     const unsigned nx = first ? 3 : 1;
     mbar_expect_tx(bar, nx * (fz::kXBytes + fz::kPBytes) + (NOB ? 0u : fz::kBBytes + fz::kBPBytes));
-    for (int p = sp + 2 - (int)nx; p <= sp + 1; ++p) tma_load_3d(sm + xpair(p), &M.xv, xc0, 2 * p + 1, 0, bar);
-    for (int r = sp + 3 - (int)nx; r <= sp + 2; ++r) tma_load_2d(sm + prow(r), &M.xp, pc0, r, bar);
+    for (int p = sp + 2 - (int)nx; p <= sp + 1; ++p) tma_load_3d(sm + rz_xpair(p), &M.xv, xc0, 2 * p + 1, 0, bar);
+    for (int r = sp + 3 - (int)nx; r <= sp + 2; ++r) tma_load_2d(sm + rz_prow(r), &M.xp, pc0, r, bar);
     if (!NOB) {
       tma_load_3d(sm + rz_bpair(sp), &M.bv, xc0 + 2, 2 * sp + 1, 0, bar);
       tma_load_2d(sm + RingRz::bp(sp + 1), &M.bp, kx0 - 2, sp + 1, bar);
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(fz::kNT, 2) k_residual_strip(const ResidArgs R
   double rc_carry[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // MODE 1: open coarse rows sp-1 .. sp+1
   double pc_carry[2] = {0.0, 0.0};                              // MODE 1: open coarse pressure rows
   int slot = 0;                                                 // (sp - spB) % 3
-  RingFzS S = RingFzS::at(spB);
+  RingSlots<rz::XPR, rz::OXS> S = RingSlots<rz::XPR, rz::OXS>::at(spB);
   for (int sp = spB; sp <= spE; ++sp) {
     const RingRzStep rg{S, sp};
     mbar_wait(&bars[slot], (phases >> slot) & 1u);
@@ -223,7 +228,7 @@ inline int launch_residual_strip(const LevelGeom& g, const LevelGeom* gc, const 
   }
   FusedMaps M;
   std::memset(&M, 0, sizeof(M));
-  if (!make_vel_map(&M.xv, g, x) || !make_p_map(&M.xp, g, x, fz::PXW)) return -2;
+  if (!make_vel_map(&M.xv, g, x, fz::WX) || !make_p_map(&M.xp, g, x, fz::PXW)) return -2;
   if (b && (!make_vel_map(&M.bv, g, b) || !make_p_map(&M.bp, g, b, fz::PWID))) return -2;
   const int ncover = (int)std::max<int64_t>(g.pu / 2, g.pp);
   const int nstrips = (ncover + fz::kNOUT - 1) / fz::kNOUT;

@@ -368,31 +368,43 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
 //    strip edge (2 patch columns and 7 lattice columns per 124 node columns).
 // =============================================================================
 namespace fz {
-// strip geometry: 4 warps x 32 patch columns; warp w covers patches 30w .. 30w+31
+// strip geometry: kWarps warps x 32 patch columns; warp w covers patches 30w .. 30w+31
 // of the strip and owns the middle 30 (lanes 0 and 31 are ghosts), so warps
-// accumulate independently.  Strip = 122 distinct patches, 120 owned node columns.
-constexpr int kNT = 128, kWarps = kNT / 32, kOWN = 30, kNOUT = kWarps * kOWN;
-constexpr int W = 256;            // ring row width (doubles): x columns xc0..xc0+255, r/b columns rc0..rc0+255
-constexpr int PWID = 128;         // b_p / r_p row width: node columns from kx0-2
-constexpr int PXW = 136;          // p ring box width: node columns pc0 = kx0-4 .. kx0+131
-constexpr int PXS = 144;          // p ring row stride (TMA smem destinations are 128-byte aligned)
+// accumulate independently.  Strip = 30 kWarps + 2 distinct patches, 30 kWarps owned
+// node columns.  Default 2 warps (SVK_STRIP_THREADS=64): 4 CTAs/SM, barriers over
+// 2 warps only (measured 3.5% faster than 4-warp strips at 2 CTAs/SM).
+#ifndef SVK_STRIP_THREADS
+#define SVK_STRIP_THREADS 64
+#endif
+constexpr int kNT = SVK_STRIP_THREADS, kWarps = kNT / 32, kOWN = 30, kNOUT = kWarps * kOWN;
+constexpr int kMinB = 256 / kNT;  // CTAs per SM the rings and registers are sized for
+constexpr int W = 2 * kNT;        // ring row width (doubles): x columns xc0..xc0+W-1, r/b columns rc0..rc0+W-1
+constexpr int PWID = kNT;         // b_p / r_p row width: node columns from kx0-2
+constexpr int PXW = kNT + 8;      // p ring box width: node columns pc0 = kx0-4 .. kx0+kNT+3
+constexpr int PXS = (PXW + 15) / 16 * 16;  // p ring row stride (TMA smem destinations are 128-byte aligned)
 // (TMA box starts must be 16-byte aligned in the innermost dimension: every
 //  box origin here is an even column.)  Ring depths let warps drift up to one
 //  step apart with a single barrier per step (see the WAR notes in the kernel).
-constexpr int XPR = 6;            // x ring: row PAIRS (2p+1, 2p+2), each [comp][2 rows][W]
+// x ring: row PAIRS (2p+1, 2p+2), each [comp][2 rows][WX].  The residual of the
+// last ghost patch column reads x up to two lattice columns beyond 2 kNT, which
+// 128-thread strips cover with idle threads; narrower strips get 4 extra columns
+// (TMA boxes stop at 256, hence none for 128; 4 keeps pairs 128-byte aligned).
+constexpr int WX = kNT >= 128 ? W : W + 4;
+constexpr int XPR = 6;
 constexpr int PR = 8;             // p ring rows
 constexpr int BPR = 2;            // b ring row pairs
 constexpr int RR = 7;             // residual ring rows, each [comp][W]
 constexpr int RPR = 4;            // pressure-residual ring rows
 constexpr int OXS = 0;
-constexpr int OPS = OXS + XPR * 4 * W;
+constexpr int OPS = OXS + XPR * 4 * WX;
 constexpr int OBS = OPS + PR * PXS;
 constexpr int OBP = OBS + BPR * 4 * W;
 constexpr int ORS = OBP + 2 * PWID;
 constexpr int ORP = ORS + RR * 2 * W;
 constexpr int OMB = ORP + RPR * PWID;  // 2 mbarriers
 constexpr int kSmemBytes = (OMB + 2) * 8;
-constexpr unsigned kXBytes = 4 * W * 8, kPBytes = PXW * 8, kBBytes = 4 * W * 8, kBPBytes = PWID * 8;
+constexpr unsigned kXBytes = 4 * WX * 8, kPBytes = PXW * 8, kBBytes = 4 * W * 8, kBPBytes = PWID * 8;
+static_assert(kMinB * (kSmemBytes + 1024) <= 232448, "kMinB sweep CTAs per SM");
 }  // namespace fz
 
 struct FusedArgs {
@@ -448,10 +460,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 // ring offsets (doubles from the smem base)
-__device__ __forceinline__ int xpair(int p) { return fz::OXS + pmod(p, fz::XPR) * 4 * fz::W; }
+__device__ __forceinline__ int xpair(int p) { return fz::OXS + pmod(p, fz::XPR) * 4 * fz::WX; }
 // x lattice row j, component c: pair (j-1)>>1, row-in-pair (j-1)&1, layout [comp][row][W]
 __device__ __forceinline__ int xrow(int j, int c) {
-  return xpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
+  return xpair((j - 1) >> 1) + c * 2 * fz::WX + ((j - 1) & 1) * fz::WX;
 }
 __device__ __forceinline__ int prow(int r) { return fz::OPS + (r & 7) * fz::PXS; }
 __device__ __forceinline__ int bpair(int p) { return fz::OBS + (p & 1) * 4 * fz::W; }
@@ -559,21 +571,22 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
 // Ring slots of one sweep step sp, maintained incrementally by the kernel (no
 // division by the non-power-of-two ring depths inside the step): xq = slot of x
 // pair sp-1, rq = residual-ring slot of lattice row 2sp-2.
-struct RingFzS {
+template <int NXP, int OX>  // x ring: NXP pairs of width fz::WX at offset OX
+struct RingSlots {
   int xq, rq;
-  __device__ __forceinline__ static RingFzS at(int sp) { return RingFzS{pmod(sp - 1, fz::XPR), pmod(2 * sp - 2, fz::RR)}; }
+  __device__ __forceinline__ static RingSlots at(int sp) { return RingSlots{pmod(sp - 1, NXP), pmod(2 * sp - 2, fz::RR)}; }
   __device__ __forceinline__ void advance() {
-    xq = xq == fz::XPR - 1 ? 0 : xq + 1;
+    xq = xq == NXP - 1 ? 0 : xq + 1;
     rq = rq + 2 >= fz::RR ? rq + 2 - fz::RR : rq + 2;
   }
   // x pair sp-1+d (d in -1..2)
   __device__ __forceinline__ int xpair_d(int d) const {
     int q = xq + d;
-    q = q >= fz::XPR ? q - fz::XPR : (q < 0 ? q + fz::XPR : q);
-    return fz::OXS + q * 4 * fz::W;
+    q = q >= NXP ? q - NXP : (q < 0 ? q + NXP : q);
+    return OX + q * 4 * fz::WX;
   }
   // lattice row j = 2sp+r (r in -3..4): pair sp + ((r-1)>>1) = sp-1 + d
-  __device__ __forceinline__ int xr(int r, int c) const { return xpair_d(((r - 1) >> 1) + 1) + c * 2 * fz::W + ((r - 1) & 1) * fz::W; }
+  __device__ __forceinline__ int xr(int r, int c) const { return xpair_d(((r - 1) >> 1) + 1) + c * 2 * fz::WX + ((r - 1) & 1) * fz::WX; }
   // residual ring row 2sp-2+o (o in 0..6)
   __device__ __forceinline__ int rr(int o, int c) const {
     int q = rq + o;
@@ -581,6 +594,7 @@ struct RingFzS {
     return fz::ORS + q * 2 * fz::W + c * fz::W;
   }
 };
+using RingFzS = RingSlots<fz::XPR, fz::OXS>;
 // adapter for fused_residual_vals: rows addressed through the step's slots
 struct RingFzStep {
   RingFzS S;
@@ -655,7 +669,7 @@ __device__ __forceinline__ void inv_transform(double (&v)[25]) {
 namespace svk {
 
 template <bool XZERO>
-__global__ void __launch_bounds__(fz::kNT, 2) k_vanka_fused(const FusedArgs A, const FusedFactors F,
+__global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedArgs A, const FusedFactors F,
                                                             const __grid_constant__ FusedMaps M) {
   extern __shared__ __align__(1024) double sm[];
   const LevelGeom& g = A.g;
@@ -860,7 +874,7 @@ __device__ __forceinline__ int z0_brow(int j, int c) {
 }
 __device__ __forceinline__ int z0_bprow(int r) { return fz0::OBP + (r & 3) * fz::PWID; }
 
-__global__ void __launch_bounds__(fz::kNT, 2) k_vanka_zero(const FusedArgs A, const FusedFactors F,
+__global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedArgs A, const FusedFactors F,
                                                             const __grid_constant__ FusedMaps M) {
   extern __shared__ __align__(1024) double sm[];
   const LevelGeom& g = A.g;
@@ -994,7 +1008,7 @@ inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const doubl
 // chunk height: about `waves` full waves of 2 CTAs per SM over the strips
 inline int fused_chunk(const LevelGeom& g, int nstrips, int nsm) {
   const int rows = g.r1 - g.r0;
-  const int resident = 2 * nsm;
+  const int resident = fz::kMinB * nsm;
   static const double target = [] {  // node rows per CTA the wave count aims at (SVK_CHUNK_ROWS: tuning aid)
     const char* e = std::getenv("SVK_CHUNK_ROWS");
     return e ? std::atof(e) : 64.0;
@@ -1024,12 +1038,12 @@ inline PFN_encodeTiled get_encode() {
   return fn;
 }
 // velocity planes of a vector: dims {lat cols, lat rows, 2 comps}; box {256, 2, 2}
-inline bool make_vel_map(CUtensorMap* m, const LevelGeom& g, const double* v) {
+inline bool make_vel_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsigned boxw = fz::W) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.lat, (cuuint64_t)g.lat, 2};
   const cuuint64_t strides[2] = {(cuuint64_t)g.pu * 8, (cuuint64_t)(g.ouy - g.oux) * 8};
-  const cuuint32_t box[3] = {fz::W, 2, 2};
+  const cuuint32_t box[3] = {boxw, 2, 2};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(v + g.oux), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1067,7 +1081,7 @@ inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int s
   FusedMaps M;
   std::memset(&M, 0, sizeof(M));
   if (!make_vel_map(&M.bv, g, b) || !make_p_map(&M.bp, g, b, fz::PWID)) return -2;
-  if (xin && (!make_vel_map(&M.xv, g, xin) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
+  if (xin && (!make_vel_map(&M.xv, g, xin, fz::WX) || !make_p_map(&M.xp, g, xin, fz::PXW))) return -2;
   const dim3 grid(nstrips, (g.r1 - g.r0 + A.chunk - 1) / A.chunk);
   if (xin) launch_pdl(k_vanka_fused<false>, grid, dim3(fz::kNT), fz::kSmemBytes, s, A, F, M);
   else launch_pdl(k_vanka_zero, grid, dim3(fz::kNT), fz0::kSmemBytes, s, A, F, M);
