@@ -52,6 +52,13 @@
  * a rank's slab are library-managed scratch.  svk_fgmres / svk_vcycle /
  * svk_vanka_sweep / svk_residual / svk_matvec must be called by all ranks
  * together (they communicate).  svk_allgather assembles a full vector.
+ *
+ * ENVIRONMENT (read once per process; tuning and test aids, results unchanged):
+ *   SVK_PDL=0          launch kernels without programmatic dependent launch;
+ *   SVK_CHUNK_ROWS=n   node rows per CTA the strip kernels' wave sizing aims at
+ *                      (default 64);
+ *   SVK_POISON_HALO=1  NaN-fill rows beyond the halo after each exchange (tests).
+ * Compile time: -DSVK_STRIP_THREADS=64|128 (threads per strip CTA, default 64).
  */
 #ifndef SVK_H_
 #define SVK_H_
