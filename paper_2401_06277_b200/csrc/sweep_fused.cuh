@@ -346,26 +346,26 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
 //   x_out = x_in + W sum_i V_i^T A_i^{-1} V_i (b - A x_in)
 //
 // Layout of the work ("owner computes", no atomics, deterministic):
-//  * a CTA of kNT = 128 threads owns a STRIP of kNOUT = 120 node columns
-//    [kx0, kx0+124) and a CHUNK of node rows [y0, y1); it streams upward
-//    through the chunk one node row (= one patch row = two lattice rows) per
-//    step, keeping rings of rows in shared memory:
-//      x ring (9 lattice rows, both components), p ring (4 node rows),
-//      residual ring (6 lattice rows), pressure-residual ring (2 rows),
-//      accumulator ring (6 lattice rows);
-//    every ring row is split by column parity, so thread t touches
-//    consecutive doubles (no bank conflicts).
-//  * step s: (1) prefetch the x / p rows of step s+1 (cp.async, zero-filled
-//    outside the domain); (2) residual r = b - A x on lattice rows 2s+1, 2s+2
-//    (thread t: lattice columns rc0+2t, rc0+2t+1) and the pressure residual on
-//    node row s+1; (3) thread t solves patch (kx0-1+t, s) exactly -- generic
-//    patches with the parity-blocked Schur form, boundary patches with their
-//    dense 51x51 group inverse -- and adds W-less contributions into the
-//    accumulator in three conflict-free phases (own columns, left neighbour's,
-//    right neighbour's); (4) lattice rows 2s-2, 2s-1 are now complete: write
-//    x_out = x_in + w * acc for the owned columns.
-//  * patches and residuals are recomputed by both neighbouring strips at a
-//    strip edge (2 patch columns and 7 lattice columns per 124 node columns).
+//  * a CTA of kNT threads (default 64 = 2 warps) owns a STRIP of kNOUT = 30 kWarps
+//    node columns starting at kx0 and a CHUNK of node rows [y0, y1); it streams
+//    upward through the chunk one node row (= one patch row = two lattice rows)
+//    per step, keeping rings of rows in shared memory, filled by TMA one step
+//    ahead (out-of-range rows / columns zero-filled) and completed on two
+//    mbarriers: x (6 row pairs, both components), p (8 node rows), b (2 pairs),
+//    b_p (2 rows), residual (7 lattice rows), pressure residual (4 rows).
+//  * step s: (1) thread 0 issues the TMA loads of step s+1; (2) residual
+//    r = b - A x on lattice rows 2s+1, 2s+2 (thread t: lattice columns rc0+2t,
+//    rc0+2t+1, both components) and the pressure residual of node row s+1, into
+//    the residual rings; (3) one CTA barrier; (4) lane l of warp w solves patch
+//    pi = 30w + l, node column kx0-1+pi, exactly: generic patches by the
+//    symmetry-shared reflection-basis Schur solve (solve_gen.cuh), boundary
+//    patches from k_boundary_patches' output; (5) owner-computes accumulation in
+//    registers (carries over three lattice rows, neighbouring patch columns via
+//    warp shuffles; lanes 0 and 31 are ghost patches, so warps never exchange
+//    partial sums) and x_out = x_in + W sum on lattice rows 2s-2, 2s-1, which are
+//    now complete.
+//  * patches and residuals at a strip edge are recomputed by both neighbouring
+//    strips (2 patch columns per 30 kWarps node columns).
 // =============================================================================
 namespace fz {
 // strip geometry: kWarps warps x 32 patch columns; warp w covers patches 30w .. 30w+31
