@@ -61,6 +61,14 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_dfma_tflops():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_fma_tflops"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def ncu_traffic():
     """dram__bytes_read.sum + write.sum per fused-sweep launch from the committed ncu capture."""
     try:
@@ -288,6 +296,16 @@ def run_svk(args):
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md counts)",
                 "hbm": {"achieved": sweep_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sweep_gbs / hbm_peak,
                         "peak_source": hbm_src, "algorithmic_bytes": bytes_alg}}
+    # the combined roofline time max(bytes/BW, flops/FP64 peak) over the measured time,
+    # the fraction of the measured DFMA-loop rate (tools/fp64_peak), and the paper-equivalent rate
+    # (dense 51x51 patch apply, 5202 flop/patch, tab:rwf) for comparison with P:640
+    t_roof = max(bytes_alg / (hbm_peak * 1e9), flops / (FP64_PEAK_TFLOPS * 1e12))
+    roofline["roofline_time_frac"] = t_roof / t_sweep
+    dfma = measured_dfma_tflops()
+    if dfma:
+        roofline["frac_of_measured_dfma"] = {"value": achieved_tf / dfma, "measured_tflops": dfma,
+                                             "source": "profiles/r1_fp64_peak.json (tools/fp64_peak.cu)"}
+    roofline["paper_equivalent_tflops"] = 5202 * nodes / t_sweep / 1e12
 
     # end to end through the C ABI with pinned host buffers
     e2e = None
