@@ -91,14 +91,19 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_dots(const VecList V, int m
   for (int i = 0; i < MM; ++i) acc[i] = 0.0;
   const int64_t n2 = S.cum2[3];
   const double2* w2 = reinterpret_cast<const double2*>(w);
-  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = seg_index(S, q0);
-    const double2 wq = w2[q];
+  // two elements per thread and pass (as k_cgs_update); the second is masked by a
+  // zero weight vector entry at the ragged end
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += 2 * stride) {
+    const bool two = q0 + stride < n2;
+    const int64_t qa = seg_index(S, q0), qb = two ? seg_index(S, q0 + stride) : qa;
+    const double2 wa = w2[qa], wb = two ? w2[qb] : make_double2(0.0, 0.0);
 #pragma unroll
     for (int i = 0; i < MM; ++i)
       if (i < m) {
-        const double2 v = reinterpret_cast<const double2*>(V.p[i])[q];
-        acc[i] = fma(v.x, wq.x, fma(v.y, wq.y, acc[i]));
+        const double2* pv = reinterpret_cast<const double2*>(V.p[i]);
+        const double2 va = pv[qa], vb = pv[qb];
+        acc[i] = fma(vb.x, wb.x, fma(vb.y, wb.y, fma(va.x, wa.x, fma(va.y, wa.y, acc[i]))));
       }
   }
   block_reduce_store_n<MM>(acc, m, 0.0, -1, partial, gridDim.x);
@@ -113,18 +118,29 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_update(const VecList V, int
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* o2 = reinterpret_cast<double2*>(wout);
   double nrm = 0.0;
-  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = seg_index(S, q0);
-    double2 a = w2[q];
+  // two elements per thread and pass: the per-vector pointer / coefficient loads are
+  // shared and twice the basis loads are in flight
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += 2 * stride) {
+    const bool two = q0 + stride < n2;
+    const int64_t qa = seg_index(S, q0), qb = two ? seg_index(S, q0 + stride) : qa;
+    double2 a = w2[qa], b = w2[qb];
 #pragma unroll 8
     for (int i = 0; i < m; ++i) {
       const double ci = __ldg(c + i);
-      const double2 v = reinterpret_cast<const double2*>(V.p[i])[q];
-      a.x = fma(-ci, v.x, a.x);
-      a.y = fma(-ci, v.y, a.y);
+      const double2* pv = reinterpret_cast<const double2*>(V.p[i]);
+      const double2 va = pv[qa], vb = pv[qb];
+      a.x = fma(-ci, va.x, a.x);
+      a.y = fma(-ci, va.y, a.y);
+      b.x = fma(-ci, vb.x, b.x);
+      b.y = fma(-ci, vb.y, b.y);
     }
-    o2[q] = a;
+    o2[qa] = a;
     nrm = fma(a.x, a.x, fma(a.y, a.y, nrm));
+    if (two) {
+      o2[qb] = b;
+      nrm = fma(b.x, b.x, fma(b.y, b.y, nrm));
+    }
   }
   double dummy[1] = {0.0};
   block_reduce_store_n<1>(dummy, 0, nrm, 0, partial, gridDim.x);
