@@ -118,29 +118,37 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_update(const VecList V, int
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* o2 = reinterpret_cast<double2*>(wout);
   double nrm = 0.0;
-  // two elements per thread and pass: the per-vector pointer / coefficient loads are
-  // shared and twice the basis loads are in flight
+  // KE elements per thread and pass: the per-vector pointer / coefficient loads are
+  // shared and KE times the basis loads are in flight
+  constexpr int KE = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += 2 * stride) {
-    const bool two = q0 + stride < n2;
-    const int64_t qa = seg_index(S, q0), qb = two ? seg_index(S, q0 + stride) : qa;
-    double2 a = w2[qa], b = w2[qb];
-#pragma unroll 8
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += KE * stride) {
+    int64_t qq[KE];
+    bool in[KE];
+    double2 a[KE];
+#pragma unroll
+    for (int e = 0; e < KE; ++e) {
+      in[e] = q0 + e * stride < n2;
+      qq[e] = in[e] ? seg_index(S, q0 + e * stride) : seg_index(S, q0);
+      a[e] = w2[qq[e]];
+    }
+#pragma unroll 4
     for (int i = 0; i < m; ++i) {
       const double ci = __ldg(c + i);
       const double2* pv = reinterpret_cast<const double2*>(V.p[i]);
-      const double2 va = pv[qa], vb = pv[qb];
-      a.x = fma(-ci, va.x, a.x);
-      a.y = fma(-ci, va.y, a.y);
-      b.x = fma(-ci, vb.x, b.x);
-      b.y = fma(-ci, vb.y, b.y);
+#pragma unroll
+      for (int e = 0; e < KE; ++e) {
+        const double2 v = pv[qq[e]];
+        a[e].x = fma(-ci, v.x, a[e].x);
+        a[e].y = fma(-ci, v.y, a[e].y);
+      }
     }
-    o2[qa] = a;
-    nrm = fma(a.x, a.x, fma(a.y, a.y, nrm));
-    if (two) {
-      o2[qb] = b;
-      nrm = fma(b.x, b.x, fma(b.y, b.y, nrm));
-    }
+#pragma unroll
+    for (int e = 0; e < KE; ++e)
+      if (in[e]) {
+        o2[qq[e]] = a[e];
+        nrm = fma(a[e].x, a[e].x, fma(a[e].y, a[e].y, nrm));
+      }
   }
   double dummy[1] = {0.0};
   block_reduce_store_n<1>(dummy, 0, nrm, 0, partial, gridDim.x);
