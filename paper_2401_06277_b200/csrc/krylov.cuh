@@ -91,19 +91,30 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_dots(const VecList V, int m
   for (int i = 0; i < MM; ++i) acc[i] = 0.0;
   const int64_t n2 = S.cum2[3];
   const double2* w2 = reinterpret_cast<const double2*>(w);
-  // two elements per thread and pass (as k_cgs_update); the second is masked by a
-  // zero weight vector entry at the ragged end
+  // KE elements per thread and pass (as k_cgs_update); elements past the ragged end
+  // are masked by a zero weight vector entry
+  constexpr int KE = MM <= 8 ? 4 : 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += 2 * stride) {
-    const bool two = q0 + stride < n2;
-    const int64_t qa = seg_index(S, q0), qb = two ? seg_index(S, q0 + stride) : qa;
-    const double2 wa = w2[qa], wb = two ? w2[qb] : make_double2(0.0, 0.0);
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n2; q0 += KE * stride) {
+    int64_t qq[KE];
+    double2 wv[KE];
+#pragma unroll
+    for (int e = 0; e < KE; ++e) {
+      const bool in = q0 + e * stride < n2;
+      qq[e] = in ? seg_index(S, q0 + e * stride) : seg_index(S, q0);
+      wv[e] = in ? w2[qq[e]] : make_double2(0.0, 0.0);
+    }
 #pragma unroll
     for (int i = 0; i < MM; ++i)
       if (i < m) {
         const double2* pv = reinterpret_cast<const double2*>(V.p[i]);
-        const double2 va = pv[qa], vb = pv[qb];
-        acc[i] = fma(vb.x, wb.x, fma(vb.y, wb.y, fma(va.x, wa.x, fma(va.y, wa.y, acc[i]))));
+        double t = acc[i];
+#pragma unroll
+        for (int e = 0; e < KE; ++e) {
+          const double2 v = pv[qq[e]];
+          t = fma(v.x, wv[e].x, fma(v.y, wv[e].y, t));
+        }
+        acc[i] = t;
       }
   }
   block_reduce_store_n<MM>(acc, m, 0.0, -1, partial, gridDim.x);
