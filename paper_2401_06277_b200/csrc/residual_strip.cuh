@@ -115,8 +115,17 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const Res
   double pc_carry[2] = {0.0, 0.0};                              // MODE 1: open coarse pressure rows
   int slot = 0;                                                 // (sp - spB) % 3
   RingSlots<rz::XPR, rz::OXS> S = RingSlots<rz::XPR, rz::OXS>::at(spB);
+  // stencil windows rolled across steps: x rows 2sp+2..2sp+4 and p rows sp+1..sp+2
+  // of step sp are rows 0..2 / 0..1 of step sp+1, so each step loads 2 x rows and
+  // 1 p row from shared memory instead of 5 and 3
+  ResWin win;
   for (int sp = spB; sp <= spE; ++sp) {
     const RingRzStep rg{S, sp};
+    auto step_residual = [&]() {
+      if (sp == spB) load_res_win<0, 2, 0, 1>(sm, rg, sp, win);
+      load_res_win<3, 4, 2, 2>(sm, rg, sp, win);
+      return residual_from_win<false, NOB, RingRzStep, true>(sm, g, F, sp, kx0, rg, win);
+    };
     mbar_wait(&bars[slot], (phases >> slot) & 1u);
     phases ^= 1u << slot;
     // prefetch step sp+2 (x pair sp+3 -> slot of sp-3, p row sp+4 -> slot of sp-4,
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const Res
     if (MODE == 0) {
       // lattice rows 2sp+1, 2sp+2 and pressure row sp+1 straight from registers:
       // thread t in [2, 122) owns node column kx0-2+t (lattice columns 2kx, 2kx+1)
-      const ResVals V = fused_residual_vals<false, NOB, RingRzStep>(sm, g, F, sp, kx0, rg);
+      const ResVals V = step_residual();
       const int kx = kx0 - 2 + t, i0 = 2 * kx;
       if (t >= 2 && t < fz::kNOUT + 2) {
         const double sg = NOB ? -1.0 : 1.0;  // NOB: the values are -A x
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const Res
       // pressure column a/2.  1D P^T weights around fine 2C: C even: -1/8, 3/8,
       // 1, 3/8, -1/8 at offsets -3, -1, 0, 1, 3; C odd: 3/4, 1, 3/4 at -1, 0, 1;
       // pressure: 1/2, 1, 1/2 around fine node 2C'.
-      const ResVals V = fused_residual_vals<false, NOB, RingRzStep>(sm, g, F, sp, kx0, rg);
+      const ResVals V = step_residual();
       double* xb = sm + rz::ORS + (sp & 1) * 5 * fz::kNT;
       xb[0 * fz::kNT + t] = V.u[0][1];
       xb[1 * fz::kNT + t] = V.u[0][3];
@@ -205,6 +214,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const Res
     }
     slot = slot == 2 ? 0 : slot + 1;
     S.advance();
+    roll_res_win(win);
   }
   // the two last prefetches (steps spE+1, spE+2) must land before the shared memory is released
   mbar_wait(&bars[slot], (phases >> slot) & 1u);

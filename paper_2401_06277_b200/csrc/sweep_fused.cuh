@@ -494,9 +494,47 @@ struct RingFz {
 // MASK = false (the fused sweep): Dirichlet / boundary-pressure rows are not
 // masked -- generic patches, the only readers of these residuals, have windows
 // strictly inside the domain (2 <= kx, ky <= N-2), so those values are never used.
+// The stencil windows of one residual step: x rows 2sp..2sp+4 (lattice columns
+// c0-2 .. c0+2, both components) and p rows sp..sp+2 (nodes kx0-3+t .. kx0-1+t).
+struct ResWin {
+  double U[5][5], V[5][5], Pm[3][3];
+};
+// load x window rows R0..R1 and p window rows P0..P1 of step sp
+template <int R0, int R1, int P0, int P1, class RG>
+__device__ __forceinline__ void load_res_win(const double* sm, const RG& rg, int sp, ResWin& w) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int r = R0; r <= R1; ++r) {
+    const double* xu = sm + rg.x(2 * sp + r, 0) + 2 * t;
+    const double* xv = sm + rg.x(2 * sp + r, 1) + 2 * t;
+    const double2 u01 = lds2(xu), u23 = lds2(xu + 2), v01 = lds2(xv), v23 = lds2(xv + 2);
+    w.U[r][0] = u01.x; w.U[r][1] = u01.y; w.U[r][2] = u23.x; w.U[r][3] = u23.y; w.U[r][4] = xu[4];
+    w.V[r][0] = v01.x; w.V[r][1] = v01.y; w.V[r][2] = v23.x; w.V[r][3] = v23.y; w.V[r][4] = xv[4];
+  }
+#pragma unroll
+  for (int r = P0; r <= P1; ++r) {
+    const double* pr = sm + rg.p(sp + r) + t + 1;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) w.Pm[r][q] = pr[q];
+  }
+}
+// step sp -> sp+1 with the overlapping rows kept in registers (x rows 2..4 -> 0..2, p rows 1..2 -> 0..1)
+__device__ __forceinline__ void roll_res_win(ResWin& w) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      w.U[r][c] = w.U[r + 2][c];
+      w.V[r][c] = w.V[r + 2][c];
+    }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) w.Pm[r][q] = w.Pm[r + 1][q];
+}
 template <bool XZERO, bool NOB = false, class RG = RingFz, bool MASK = true>
-__device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const LevelGeom& g, const FusedFactors& F,
-                                                       int sp, int kx0, const RG& rg = RG{}) {
+__device__ __forceinline__ ResVals residual_from_win(const double* sm, const LevelGeom& g, const FusedFactors& F,
+                                                     int sp, int kx0, const RG& rg, const ResWin& w) {
   const int N = g.N, lat = g.lat, t = threadIdx.x;
   const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
@@ -509,22 +547,9 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
   for (int q = 0; q < 8; ++q) ax[q] = 0.0;
   double bu = 0.0;
   if (!XZERO) {
-    double U[5][5], V[5][5];  // window rows 2sp..2sp+4, lattice columns c0-2..c0+2 (x columns 2t..2t+4)
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const double* xu = sm + rg.x(2 * sp + r, 0) + 2 * t;
-      const double* xv = sm + rg.x(2 * sp + r, 1) + 2 * t;
-      const double2 u01 = lds2(xu), u23 = lds2(xu + 2), v01 = lds2(xv), v23 = lds2(xv + 2);
-      U[r][0] = u01.x; U[r][1] = u01.y; U[r][2] = u23.x; U[r][3] = u23.y; U[r][4] = xu[4];
-      V[r][0] = v01.x; V[r][1] = v01.y; V[r][2] = v23.x; V[r][3] = v23.y; V[r][4] = xv[4];
-    }
-    double Pm[3][3];  // p rows sp..sp+2, nodes kx0-3+t .. kx0-1+t (p ring column node - (kx0-4))
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const double* pr = sm + rg.p(sp + r) + t + 1;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) Pm[r][q] = pr[q];
-    }
+    const double (&U)[5][5] = w.U;
+    const double (&V)[5][5] = w.V;
+    const double (&Pm)[3][3] = w.Pm;
     stencil_L_sym(U, V, ax, F);  // shared-coefficient form (stencil_gen.cuh)
     const bool pint = na >= 1 && na <= N - 1 && nrow >= 1 && nrow <= N - 1;
     if (pint || !MASK) {  // B u on the interior pressure-row pattern (window = U/V)
@@ -566,6 +591,14 @@ __device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const L
   }
   R.p = (!MASK || pok) ? (NOB ? 0.0 : sm[rg.bp(nrow) + t]) - bu : 0.0;
   return R;
+}
+
+template <bool XZERO, bool NOB = false, class RG = RingFz, bool MASK = true>
+__device__ __forceinline__ ResVals fused_residual_vals(const double* sm, const LevelGeom& g, const FusedFactors& F,
+                                                       int sp, int kx0, const RG& rg = RG{}) {
+  ResWin w;
+  if (!XZERO) load_res_win<0, 4, 0, 2>(sm, rg, sp, w);
+  return residual_from_win<XZERO, NOB, RG, MASK>(sm, g, F, sp, kx0, rg, w);
 }
 // the same, stored into the residual rings (rows j0, j1 and pressure row sp+1)
 // Ring slots of one sweep step sp, maintained incrementally by the kernel (no
