@@ -652,9 +652,22 @@ __device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, c
 }
 // the same with the step's slots supplied by the caller
 __device__ __forceinline__ void fused_residual_step(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
-                                                    int kx0, const RingFzS& S) {
+                                                    int kx0, const RingFzS& S, double (&pm)[3][3], bool first) {
   const RingFzStep rg{S, sp};
-  const ResVals R = fused_residual_vals<false, false, RingFzStep, false>(sm, g, F, sp, kx0, rg);
+  ResWin win;
+  load_res_win<0, 4, 2, 2>(sm, rg, sp, win);  // x rows 0..4; p row 2 (rows 0..1 carried in pm)
+  if (first) load_res_win<0, -1, 0, 1>(sm, rg, sp, win);
+  else {
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) win.Pm[r][q] = pm[r + 1][q];
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) pm[r][q] = win.Pm[r][q];
+  const ResVals R = residual_from_win<false, false, RingFzStep, false>(sm, g, F, sp, kx0, rg, win);
   const int t = threadIdx.x;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
@@ -776,6 +789,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
     for (int b = 0; b < 2; ++b)
       wgt[a][b] = A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0);
   RingFzS S = RingFzS::at(sB);
+  double pmw[3][3];  // pressure window rolled across steps
   for (int s = sB; s <= sE; ++s) {
     // Data of step s (x pairs up to s+1, p rows up to s+2, b pair s, b_p row s+1)
     // arrived on barrier (s-sB+1)&1; prefetch step s+1 into the other one.
@@ -801,7 +815,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
       tma_load_3d(sm + bpair(s + 1), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
       tma_load_2d(sm + bprow(s + 2), &M.bp, kx0 - 2, s + 2, nbar);
     }
-    fused_residual_step(sm, A.g, F, s, kx0, S);
+    fused_residual_step(sm, A.g, F, s, kx0, S, pmw, s == sB);
     __syncthreads();
 
     // ---- patch solve (alg:vk line 2: A_i delta_i = V_i r, exactly) ----
