@@ -23,8 +23,7 @@ Output: straight-line code, deterministic (fixed order per accumulator).
 import os
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "paper_2401_06277_b200", "csrc", "solve_gen.cuh")
-OUT_ST = os.path.join(ROOT, "paper_2401_06277_b200", "csrc", "stencil_gen.cuh")
+CSRC = os.path.join(ROOT, "paper_2401_06277_b200", "csrc")
 
 
 def par(i):  # 0..2 even, 3..4 odd
@@ -156,7 +155,9 @@ def stencil_code():
     return L
 
 
-def main():
+def main(outdir=CSRC):
+    OUT = os.path.join(outdir, "solve_gen.cuh")
+    OUT_ST = os.path.join(outdir, "stencil_gen.cuh")
     L = [
         "// solve_gen.cuh -- GENERATED by tools/gen_solve.py; do not edit.",
         "// Generic-patch solve in the reflection basis with symmetry-shared",
@@ -210,4 +211,5 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+    main(sys.argv[1] if len(sys.argv) > 1 else CSRC)
