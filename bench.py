@@ -201,12 +201,16 @@ def cpu_baseline(args):
     N = args.cpu_n
     o = oracle.Oracle(N)
     b, x0 = o.problem(oracle.MMS_PAPER)
-    t0 = time.perf_counter()
-    _, its, _, _, _ = o.fgmres(b, x0, rtol=args.rtol)
-    t = time.perf_counter() - t0
-    return {"value": n_dof(N) / t, "unit": "DOF/s", "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": "one FGMRES+V(1,1)-Vanka solve of the %d^2 MMS problem to %g (%d iterations, %.1f s; "
-                      "oracle C++/OpenMP, setup excluded)" % (N, args.rtol, its, t)}
+    # repeat the solve until about 10 s of CPU work (at most 5 solves)
+    t, nsolve = 0.0, 0
+    while nsolve < 5 and (nsolve == 0 or t < 10.0):
+        t0 = time.perf_counter()
+        _, its, _, _, _ = o.fgmres(b, x0, rtol=args.rtol)
+        t += time.perf_counter() - t0
+        nsolve += 1
+    return {"value": nsolve * n_dof(N) / t, "unit": "DOF/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": "%d FGMRES+V(1,1)-Vanka solve(s) of the %d^2 MMS problem to %g (%d iterations each, %.1f s "
+                      "in total; oracle C++/OpenMP, setup excluded)" % (nsolve, N, args.rtol, its, t)}
 
 
 def run_svk(args):
