@@ -1,0 +1,51 @@
+"""Parity away from the default parameters: viscosity nu != 1 (the stencils and the
+patch factors scale with it: L = nu (M (x) K + K (x) M)), V(2,2) cycles
+(alg:mg nu1 = nu2 = 2) and another Vanka weight, each against the oracle
+built with the same parameters.  1e-12 relative as everywhere (north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+import svk_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("nu", [0.01, 7.5])
+@pytest.mark.parametrize("N", [16, 64])
+def test_viscosity_sweep_residual_vcycle(gpu, nu, N):
+    from paper_2401_06277_b200 import Solver
+    S, O = Solver(N, nu=nu), oracle.Oracle(N, nu=nu)
+    l = S.fine
+    x = svk_inputs.random_vector(N, 31)
+    b = svk_inputs.random_vector(N, 32)
+    rg = S.to_compact(S.residual(l, S.from_compact(x), S.from_compact(b))).cpu().numpy()
+    assert rel(rg, O.residual(l, x, b)) < 1e-12
+    xg = S.to_compact(S.sweep(l, S.from_compact(x), S.from_compact(b))).cpu().numpy()
+    assert rel(xg - x, O.sweep(l, x, b) - x) < 1e-12
+    bb = b.copy()
+    bb[O.dirichlet(l)] = 0.0
+    vg = S.to_compact(S.vcycle(S.from_compact(bb))).cpu().numpy()
+    assert rel(vg, O.vcycle(bb)) < 1e-12
+
+
+@pytest.mark.parametrize("N", [32, 128])
+def test_v22_and_weight(gpu, N):
+    from paper_2401_06277_b200 import Solver
+    S = Solver(N, nu_pre=2, nu_post=2, omega=0.7)
+    O = oracle.Oracle(N, nu1=2, nu2=2, omega=0.7)
+    b = svk_inputs.random_vector(N, 41)
+    b[O.dirichlet(O.fine)] = 0.0
+    x0 = svk_inputs.random_vector(N, 42)
+    vg = S.to_compact(S.vcycle(S.from_compact(b), S.from_compact(x0))).cpu().numpy()
+    vo = O.vcycle(b, x0)
+    assert rel(vg - x0, vo - x0) < 1e-12
+    bg, xg0 = S.set_problem("mms_paper")
+    rep, _ = S.fgmres(bg, xg0, rtol=1e-10, maxit=100)
+    bo, x0o = O.problem(oracle.MMS_PAPER)
+    its_o = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)[1]
+    assert abs(rep["iterations"] - its_o) <= 1, (rep["iterations"], its_o)
