@@ -49,3 +49,26 @@ def test_v22_and_weight(gpu, N):
     bo, x0o = O.problem(oracle.MMS_PAPER)
     its_o = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)[1]
     assert abs(rep["iterations"] - its_o) <= 1, (rep["iterations"], its_o)
+
+
+@pytest.mark.parametrize("N", [48, 96, 384])
+def test_coarsest_six(gpu, N):
+    """hierarchy with N0 = 6 (N = 6 * 2^k): 49 / 97 / 385 node columns, ragged against
+    the strip width (60 node columns) and the chunking"""
+    from paper_2401_06277_b200 import Solver
+    S, O = Solver(N, n_coarse=6), oracle.Oracle(N, n_coarse=6)
+    l = S.fine
+    x = svk_inputs.random_vector(N, 51)
+    b = svk_inputs.random_vector(N, 52)
+    xg = S.to_compact(S.sweep(l, S.from_compact(x), S.from_compact(b))).cpu().numpy()
+    assert rel(xg - x, O.sweep(l, x, b) - x) < 1e-12
+    bb = b.copy()
+    bb[O.dirichlet(l)] = 0.0
+    vg = S.to_compact(S.vcycle(S.from_compact(bb))).cpu().numpy()
+    assert rel(vg, O.vcycle(bb)) < 1e-12
+    if N <= 96:
+        bg, xg0 = S.set_problem("mms_paper")
+        rep, _ = S.fgmres(bg, xg0, rtol=1e-10, maxit=100)
+        bo, x0o = O.problem(oracle.MMS_PAPER)
+        its_o = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)[1]
+        assert abs(rep["iterations"] - its_o) <= 1, (rep["iterations"], its_o)
