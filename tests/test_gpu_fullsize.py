@@ -21,18 +21,21 @@ def solver(gpu):
 
 
 def structured_samples(Nn):
-    """DOFs at the places a tiled kernel gets wrong: domain edges, strip edges
-    (124-node strips), chunk rows, plus pressure nodes there."""
+    """DOFs at the places a tiled kernel gets wrong: domain edges, strip edges (60-node
+    strips of 2-warp CTAs, 120-node strips of 4-warp ones), chunk rows (64-69 node
+    rows per CTA at this size), plus pressure nodes there."""
     lat = 2 * Nn + 1
     nv = lat * lat
-    cols = sorted({1, 2, 3, 4, 5, lat - 2, lat - 3, lat - 4, lat - 5, 246, 247, 248, 249, 250, 251, 494, 495, 496, 497})
-    rows = sorted({1, 2, 3, lat - 2, lat - 3, 240, 241, 242, 243, 244, 245, 4000, 4001})
+    node_cols = [0, 1, 2, Nn - 2, Nn - 1, Nn] + [c + d for c in (60, 120, 240, 1200) for d in (-2, -1, 0, 1, 2)]
+    node_rows = [0, 1, 2, Nn - 2, Nn - 1, Nn] + [r + d for r in (64, 69, 128, 138, 2000) for d in (-1, 0, 1)]
+    cols = sorted({i for k in node_cols for i in (2 * k - 1, 2 * k, 2 * k + 1) if 1 <= i <= lat - 2})
+    rows = sorted({j for k in node_rows for j in (2 * k - 1, 2 * k, 2 * k + 1) if 1 <= j <= lat - 2})
     out = []
     for j in rows:
         for i in cols:
             out += [j * lat + i, nv + j * lat + i]
-    for ky in (0, 1, 2, 121, 122, Nn - 1, Nn):
-        for kx in (0, 1, 2, 123, 124, 125, Nn - 2, Nn):
+    for ky in node_rows:
+        for kx in node_cols:
             out.append(2 * nv + ky * (Nn + 1) + kx)
     return np.array(sorted(set(out)), dtype=np.int64)
 
