@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_residual_strip(const Res
     // b pair sp+2 -> slot of sp-2, b_p row sp+3 -> slot of sp-1): every thread has
     // passed the barrier of step sp-1, i.e. finished the residual of step sp-1.
     const int nslot = slot == 0 ? 2 : slot - 1;  // (sp + 2 - spB) % 3
-    if (t == 0) issue(sp + 2, &bars[nslot], false);
+    if (t == (((sp - spB) & 1) << 5) % fz::kNT) issue(sp + 2, &bars[nslot], false);  // issuer alternates warps
     if (MODE == 0) {
       // lattice rows 2sp+1, 2sp+2 and pressure row sp+1 straight from registers:
       // thread t in [2, 122) owns node column kx0-2+t (lattice columns 2kx, 2kx+1)

@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
     mbar_wait(&bars[bi], (phases >> bi) & 1u);
     phases ^= 1u << bi;
     uint64_t* nbar = &bars[(s - sB) & 1];
-    if (t == 0) {
+    if (t == (((s - sB) & 1) << 5) % fz::kNT) {  // the issuing lane alternates between warps
       unsigned bytes = fz::kBBytes + fz::kBPBytes + (XZERO ? 0u : fz::kXBytes + fz::kPBytes);
       mbar_expect_tx(nbar, bytes);
       if (!XZERO) {
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
     mbar_wait(&bars[bi], (phases >> bi) & 1u);
     phases ^= 1u << bi;
     __syncthreads();
-    if (t == 0) {
+    if (t == (bi << 5) % fz::kNT) {  // the issuing lane alternates between warps
       uint64_t* nbar = &bars[bi ^ 1];
       mbar_expect_tx(nbar, fz::kBBytes + fz::kBPBytes);
       tma_load_3d(sm + z0_brow(2 * s + 3, 0), &M.bv, xc0 + 2, 2 * s + 3, 0, nbar);
