@@ -75,6 +75,59 @@ __global__ void k_bt_smooth(const BtArgs a, const double* __restrict__ x, const 
   }
 }
 
+// Velocity part, two lattice columns (one even, one odd) per thread so the
+// parity -- hence the stencil, taken from the level's L2D table (the fused
+// sweep's, nu (M (x) K + K (x) M) by parity class) -- is warp-uniform and the
+// 5 x 5 loops unroll: JAC = 1: out = x + omega D^{-1} (b - L x), JAC = 0:
+// out = b - L x; Dirichlet points and padding -> 0.  grid: (pairs / 32, rows / 8, 2).
+struct L2DTab {
+  double c[2][2][5][5];
+};
+template <int JAC>
+__global__ void __launch_bounds__(256) k_bt_smooth_vel(const BtArgs a, const L2DTab T, const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ out) {
+  const LevelGeom& g = a.g;
+  const int lat = g.lat;
+  const int i0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x), j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int comp = blockIdx.z;
+  if (j >= lat || i0 >= g.pu) return;
+  const double* u = x + (comp ? g.ouy : g.oux);
+  const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i0;
+  double w[5][6];  // rows j-2 .. j+2, columns i0-2 .. i0+3 (0 outside the plane)
+#pragma unroll
+  for (int bb = 0; bb < 5; ++bb) {
+    const int jj = j - 2 + bb;
+    const bool rok = jj >= 0 && jj < lat;
+#pragma unroll
+    for (int aa = 0; aa < 6; ++aa) {
+      const int ii = i0 - 2 + aa;
+      w[bb][aa] = (rok && ii >= 0 && ii < lat) ? u[(int64_t)jj * g.pu + ii] : 0.0;
+    }
+  }
+  const int pj = j & 1;
+  double r[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {  // e = column parity of point i0 + e
+    double s = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < 5; ++bb)
+#pragma unroll
+      for (int aa = 0; aa < 5; ++aa) s = fma(T.c[pj][e][bb][aa], w[bb][aa + e], s);
+    r[e] = s;
+  }
+  const bool jin = j >= 1 && j <= lat - 2;
+  double res[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int i = i0 + e;
+    const bool in = jin && i >= 1 && i <= lat - 2;
+    const double rv = in ? b[o + e] - r[e] : 0.0;
+    res[e] = JAC ? (in ? fma(a.omega * a.dinv[pj][e], rv, x[o + e]) : 0.0) : rv;
+  }
+  if (i0 + 1 < g.pu) *reinterpret_cast<double2*>(out + o) = make_double2(res[0], res[1]);
+  else out[o] = res[0];
+}
+
 // BT right-hand sides on the finest level: MODE 0: out = (0, 0, -r_p);
 // MODE 1: out_u = r_u - B^T dp (dp = the pressure plane of x), out_p = 0.
 template <int MODE>

@@ -484,11 +484,15 @@ int op_blk_mg(svk_ctx* ctx, int l, int part, const double* b, double* x, cudaStr
   dim3 grid = plane_grid(g);
   grid.z = part ? 1 : 2;
   if (part) grid = dim3((unsigned)((g.pp + 31) / 32), (unsigned)((g.N + 1 + 7) / 8), 1);
+  L2DTab tab;
+  std::memcpy(&tab, F.L2D, sizeof(tab));
+  const dim3 vblk(32, 8), vgrid((unsigned)((g.pu / 2 + 31) / 32), (unsigned)((g.lat + 7) / 8), 2);
   auto smooth = [&]() -> int {
     const double* src = x;
     double* dst = ctx->ws_t[l];
     for (int k = 0; k < c.bt_nu; ++k) {
-      k_bt_smooth<1><<<grid, kPlaneBlock, 0, s>>>(a, src, b, dst);
+      if (part == 0) k_bt_smooth_vel<1><<<vgrid, vblk, 0, s>>>(a, tab, src, b, dst);
+      else k_bt_smooth<1><<<grid, kPlaneBlock, 0, s>>>(a, src, b, dst);
       CKL();
       ++ctx->launches;
       double* nsrc = dst;
@@ -499,7 +503,8 @@ int op_blk_mg(svk_ctx* ctx, int l, int part, const double* b, double* x, cudaStr
     return SVK_OK;
   };
   TRY(smooth());
-  k_bt_smooth<0><<<grid, kPlaneBlock, 0, s>>>(a, x, b, ctx->ws_r[l]);
+  if (part == 0) k_bt_smooth_vel<0><<<vgrid, vblk, 0, s>>>(a, tab, x, b, ctx->ws_r[l]);
+  else k_bt_smooth<0><<<grid, kPlaneBlock, 0, s>>>(a, x, b, ctx->ws_r[l]);
   CKL();
   const LevelGeom& gc = ctx->g[l - 1];
   dim3 cg = plane_grid(gc);
