@@ -125,6 +125,68 @@ __global__ void k_bs_update(const BsArgs a, const double* __restrict__ xin, cons
   }
 }
 
+// The same update with two lattice columns (even, odd) per thread and one row per
+// warp, so the B^T stencil shape (parity) is warp-uniform: no divergence between
+// neighbouring threads and unrolled pressure taps.  z = 0, 1: velocity planes;
+// z = 2: the pressure plane (nodes 2p, 2p+1 of row j).  grid: (pairs / 32, rows / 8, 3).
+__global__ void __launch_bounds__(256) k_bs_update2(const BsArgs a, const double* __restrict__ xin,
+                                                    const double* __restrict__ r, const double* __restrict__ dp,
+                                                    double* __restrict__ xout) {
+  const LevelGeom& g = a.g;
+  const int plane = blockIdx.z;
+  const int pr = blockIdx.x * blockDim.x + threadIdx.x;  // column pair
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int N = g.N, lat = g.lat;
+  if (plane == 2) {
+    if (j > N) return;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 2 * pr + e;
+      if (i >= g.pp) continue;
+      const int64_t o = p_at(g, i, j);
+      xout[o] = i > N ? 0.0 : fma(a.omega_r, dp[(int64_t)j * g.pp + i], xin[o]);
+    }
+    return;
+  }
+  const int i0 = 2 * pr;
+  if (j >= lat || i0 >= g.pu) return;
+  const int64_t o = (plane ? g.ouy : g.oux) + (int64_t)j * g.pu + i0;
+  const int pj = j & 1;
+  // pressure window: node rows ky0 .. ky0 + 2 (row parity odd: 2 rows), columns pr-1 .. pr+1
+  const int ky0 = pj ? (j - 1) >> 1 : (j >> 1) - 1;
+  double P[3][3];
+#pragma unroll
+  for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+    for (int tx = 0; tx < 3; ++tx) {
+      const int ky = ky0 + ty, kx = pr - 1 + tx;
+      const bool ok = !a.su && ky >= 0 && ky <= N && kx >= 0 && kx <= N && (ty < 2 || !pj);
+      P[ty][tx] = ok ? dp[(int64_t)ky * g.pp + kx] : 0.0;
+    }
+  double res[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {  // e = column parity of point i0 + e
+    const int i = i0 + e;
+    double bt = 0.0;
+#pragma unroll
+    for (int ty = 0; ty < 3; ++ty) {
+      if (pj && ty == 2) continue;
+      const double cy = plane == 0 ? c_st.CC[pj][ty] : c_st.GC[pj][ty];
+      double tsum = 0.0;
+#pragma unroll
+      for (int tx = 0; tx < 3 - e; ++tx)  // even point: nodes pr-1 .. pr+1; odd: pr .. pr+1
+        tsum += (plane == 0 ? c_st.GC[e][tx] : c_st.CC[e][tx]) * P[ty][tx + e];
+      bt += cy * tsum;
+    }
+    bt *= -g.h;
+    if (i >= lat) res[e] = 0.0;
+    else if (i == 0 || j == 0 || i == lat - 1 || j == lat - 1) res[e] = xin[o + e];
+    else res[e] = fma(a.omega_r * a.inv_t * a.dinv[pj][e], r[o + e] - bt, xin[o + e]);
+  }
+  if (i0 + 1 < g.pu) *reinterpret_cast<double2*>(xout + o) = make_double2(res[0], res[1]);
+  else xout[o] = res[0];
+}
+
 // ---- host: S class stencils of one level --------------------------------------
 // 1D assembled entries from the element tables (host twins of k1/m1/c1/g1 in
 // stencil.cuh): h K, M / h, C / h, G.

@@ -442,7 +442,10 @@ int op_bs(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout,
     CKL();
     dp = out;
   }
-  k_bs_update<<<plane_grid(g), kPlaneBlock, 0, s>>>(a, xin, r, dp, xout);
+  {
+    const dim3 blk(32, 8), grd((unsigned)((std::max<int64_t>(g.pu, g.pp) / 2 + 32) / 32), (unsigned)((g.lat + 7) / 8), 3);
+    k_bs_update2<<<grd, blk, 0, s>>>(a, xin, r, dp, xout);
+  }
   CKL();
   ctx->launches += 3 + c.jacobi_sweeps;
   return SVK_OK;
