@@ -107,12 +107,19 @@ __global__ void __launch_bounds__(256) k_bt_smooth_vel(const BtArgs a, const L2D
   const int pj = j & 1;
   double r[2];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {  // e = column parity of point i0 + e
+  for (int e = 0; e < 2; ++e) {  // e = column parity of point i0 + e (row parity: warp-uniform branch)
     double s = 0.0;
+    if (pj) {
 #pragma unroll
-    for (int bb = 0; bb < 5; ++bb)
+      for (int bb = 0; bb < 5; ++bb)
 #pragma unroll
-      for (int aa = 0; aa < 5; ++aa) s = fma(T.c[pj][e][bb][aa], w[bb][aa + e], s);
+        for (int aa = 0; aa < 5; ++aa) s = fma(T.c[1][e][bb][aa], w[bb][aa + e], s);
+    } else {
+#pragma unroll
+      for (int bb = 0; bb < 5; ++bb)
+#pragma unroll
+        for (int aa = 0; aa < 5; ++aa) s = fma(T.c[0][e][bb][aa], w[bb][aa + e], s);
+    }
     r[e] = s;
   }
   const bool jin = j >= 1 && j <= lat - 2;
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(256) k_bt_smooth_vel(const BtArgs a, const L2D
     const int i = i0 + e;
     const bool in = jin && i >= 1 && i <= lat - 2;
     const double rv = in ? b[o + e] - r[e] : 0.0;
-    res[e] = JAC ? (in ? fma(a.omega * a.dinv[pj][e], rv, x[o + e]) : 0.0) : rv;
+    res[e] = JAC ? (in ? fma(a.omega * (pj ? a.dinv[1][e] : a.dinv[0][e]), rv, x[o + e]) : 0.0) : rv;
   }
   if (i0 + 1 < g.pu) *reinterpret_cast<double2*>(out + o) = make_double2(res[0], res[1]);
   else out[o] = res[0];

@@ -50,8 +50,11 @@ struct Seg3 {
   int64_t cum2[4];
 };
 __device__ __forceinline__ int64_t seg_index(const Seg3& S, int64_t q) {
-  const int s = q < S.cum2[1] ? 0 : (q < S.cum2[2] ? 1 : 2);
-  return S.off2[s] + (q - S.cum2[s]);
+  // selects instead of a runtime index into the parameter (which would copy S to local memory)
+  const bool a = q < S.cum2[1], b = q < S.cum2[2];
+  const int64_t off = a ? S.off2[0] : (b ? S.off2[1] : S.off2[2]);
+  const int64_t base = a ? 0 : (b ? S.cum2[1] : S.cum2[2]);
+  return off + (q - base);
 }
 
 template <int MM>

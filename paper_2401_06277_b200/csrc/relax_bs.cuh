@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) k_bs_update2(const BsArgs a, const double
     bt *= -g.h;
     if (i >= lat) res[e] = 0.0;
     else if (i == 0 || j == 0 || i == lat - 1 || j == lat - 1) res[e] = xin[o + e];
-    else res[e] = fma(a.omega_r * a.inv_t * a.dinv[pj][e], r[o + e] - bt, xin[o + e]);
+    else res[e] = fma(a.omega_r * a.inv_t * (pj ? a.dinv[1][e] : a.dinv[0][e]), r[o + e] - bt, xin[o + e]);
   }
   if (i0 + 1 < g.pu) *reinterpret_cast<double2*>(xout + o) = make_double2(res[0], res[1]);
   else xout[o] = res[0];
