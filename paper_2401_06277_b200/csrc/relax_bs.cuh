@@ -17,7 +17,7 @@
 // node to the boundary (0, 1, 2, interior, N-2, N-1, N -> 7 x 7 classes), built
 // once per level on the host from the exact 1D element matrices.
 // Kernels: residual (k_residual_strip) -> k_bs_rhs -> nj x k_schur_jacobi ->
-// k_bs_update.  All HBM-bound plane kernels; the comparators are not the hot path.
+// k_bs_update2.  Plane kernels; the comparators are not the hot path.
 #pragma once
 #include "kernels_common.cuh"
 
@@ -98,36 +98,9 @@ __global__ void k_schur_jacobi(LevelGeom g, const double* __restrict__ st, doubl
 }
 
 // x_out = x_in + omega_r (du, dp),  du = (1/t) D^{-1} (r_u - [B^T dp]) on non-Dirichlet DOFs
-__global__ void k_bs_update(const BsArgs a, const double* __restrict__ xin, const double* __restrict__ r,
-                            const double* __restrict__ dp, double* __restrict__ xout) {
-  const LevelGeom& g = a.g;
-  const int plane = blockIdx.z;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int N = g.N, lat = g.lat;
-  if (plane < 2) {
-    if (j >= lat || i >= g.pu) return;
-    const int64_t o = (plane ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-    if (i >= lat) {
-      xout[o] = 0.0;
-      return;
-    }
-    if (i == 0 || j == 0 || i == lat - 1 || j == lat - 1) {
-      xout[o] = xin[o];
-      return;
-    }
-    const double bt = a.su ? 0.0 : gradp_at(dp, g.pp, i, j, plane, g.h);
-    xout[o] = fma(a.omega_r * a.inv_t * a.dinv[j & 1][i & 1], r[o] - bt, xin[o]);
-  } else {
-    if (j > N || i >= g.pp) return;
-    const int64_t o = p_at(g, i, j);
-    xout[o] = i > N ? 0.0 : fma(a.omega_r, dp[(int64_t)j * g.pp + i], xin[o]);
-  }
-}
-
-// The same update with two lattice columns (even, odd) per thread and one row per
-// warp, so the B^T stencil shape (parity) is warp-uniform: no divergence between
-// neighbouring threads and unrolled pressure taps.  z = 0, 1: velocity planes;
+// Two lattice columns (even, odd) per thread and one row per warp, so the B^T
+// stencil shape (parity) is warp-uniform: no divergence between neighbouring
+// threads and unrolled pressure taps.  z = 0, 1: velocity planes;
 // z = 2: the pressure plane (nodes 2p, 2p+1 of row j).  grid: (pairs / 32, rows / 8, 3).
 __global__ void __launch_bounds__(256) k_bs_update2(const BsArgs a, const double* __restrict__ xin,
                                                     const double* __restrict__ r, const double* __restrict__ dp,
