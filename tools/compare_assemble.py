@@ -32,6 +32,8 @@ for p in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "compare_sweep_*_%s.j
     variants.append({"N": int(n), "sweep_impl": impl, "iterations": d["iterations"],
                      "time_to_solve_s": d["time_to_solve_s"], "sweep_ms": d["sweep"]["ms"],
                      "t_precond_s": d["t_vcycle_s"], "t_orth_s": d["t_orth_s"]})
+if not runs:
+    sys.exit("no compare_*_%s.json in gpurun_out/: profiles/r1_compare.json left unchanged" % tag)
 old["runs"] = runs
 old["vanka_variants"]["runs"] = variants
 old["measured"] = "round 1, %s (kernel v9: symmetry-shared coefficients)" % tag
