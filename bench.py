@@ -18,7 +18,7 @@ sweep  = the finest-level Vanka sweeps inside the timed solves (CUDA events on t
 e2e    = the same solve through svk_solve_host with pinned HOST buffers (H2D of
          b and x0, D2H of x inside the timed region).
 --impl reference  times the CPU oracle (oracle/, C++ + OpenMP, fp64) on a bounded
-         sample of the same workload (a 256^2 solve per step) on the host cores.
+         sample of the same workload (a 512^2 solve per step, the cpu_baseline's size) on the host cores.
 Multi-GPU (N > 1, torchrun): `--mode slabs` (default) splits the ONE 4096^2
 problem into N row slabs (libsvk multi-GPU mode over NCCL: halo exchanges,
 coarse-level agglomeration, all-reduced Krylov dots; strong scaling);
@@ -163,7 +163,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong" if world > 1 and args.mode == "slabs" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, world),
+        "config": dict(config_dict(args, world, n=N),
+                       bounded_sample_of=config_dict(args, world)["workload"],
+                       sample_note="the CPU oracle solves the N=%d instance of the same workload per step (a 4096^2 "
+                                   "oracle solve takes tens of minutes); value is its DOF/s" % N),
         "iterations": its,
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "oracle",
                          "sample": "FGMRES+V(1,1)-Vanka solve of the %d^2 MMS problem per step (oracle C++/OpenMP, "
@@ -177,8 +180,10 @@ def run_reference(args):
 RELAX_NAMES = {"vanka": "Vanka", "bs": "Braess-Sarazin", "su": "Schur-Uzawa"}
 
 
-def config_dict(args, world=1):
+def config_dict(args, world=1, n=None):
     relax = getattr(args, "relax", "vanka")
+    if n is not None:  # the size actually run (reference arm: the oracle's bounded sample)
+        args = argparse.Namespace(**dict(vars(args), n=n))
     if getattr(args, "precond", "mg") == "bt":
         wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10) + block-triangular "
               "preconditioner (3 V(3,3) Jacobi cycles per block)" % (args.n, args.n))
@@ -381,7 +386,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=512)
-    ap.add_argument("--ref-n", type=int, default=256)
+    ap.add_argument("--ref-n", type=int, default=512)
     ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs")
     ap.add_argument("--agglom", type=int, default=64)
     ap.add_argument("--relax", choices=["vanka", "bs", "su"], default="vanka",

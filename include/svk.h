@@ -14,7 +14,9 @@
  *
  * ---------------------------------------------------------------------------
  * VECTORS.  Every vector argument is a caller-owned DEVICE buffer of double
- * (8-byte aligned; 256-byte aligned recommended) holding one level's vector
+ * (16-byte aligned -- the kernels use 16-byte vector and TMA accesses, and a
+ * less aligned pointer is rejected with SVK_ERR_INVALID; 256-byte aligned
+ * recommended) holding one level's vector
  * in the PITCHED layout reported by svk_level_info():
  *   u_x plane at off_ux: (2N+1) rows (y) of pitch_u doubles, column i = x index
  *   u_y plane at off_uy: same shape
@@ -43,7 +45,10 @@
  * SVK_ERR_NONFINITE: FGMRES met NaN/Inf.
  *
  * THREADING.  One context per device; calls on one context must not overlap
- * (scratch is per context).  Different contexts are independent.
+ * (scratch is per context).  Different contexts are independent: every call
+ * taking a context runs on cfg.device (the caller's current device is
+ * restored on return), and C++ exceptions never cross this boundary (they map
+ * to SVK_ERR_ALLOC / SVK_ERR_INVALID with a message).
  *
  * MULTI-GPU (nranks > 1).  Every rank creates one context with the same
  * configuration except `rank`.  The finest levels are split into row slabs;
@@ -52,6 +57,9 @@
  * a rank's slab are library-managed scratch.  svk_fgmres / svk_vcycle /
  * svk_vanka_sweep / svk_residual / svk_matvec must be called by all ranks
  * together (they communicate).  svk_allgather assembles a full vector.
+ * svk_restrict / svk_prolong_add do not exchange halos: on a distributed level
+ * they compute the rank's owned rows from the rows it already holds, so the
+ * caller must pass inputs whose halo rows are current (as svk_vcycle does).
  *
  * ENVIRONMENT (read once per process; tuning and test aids, results unchanged):
  *   SVK_PDL=0          launch kernels without programmatic dependent launch;

@@ -367,6 +367,32 @@ void residual(const Level& L, const double* x, const double* b, double* r) {
 // LU-factored once ("inverting each patch matrix ahead of time");
 // bitwise-identical A_i share one factorisation (tuned Vanka).
 // --------------------------------------------------------------------------
+// A_i = V_i A V_i^T of patch p (row-major n x n, n = the patch's DOF count):
+// entry (r, c) = A[pdof[r], pdof[c]] from the global CSR.  The patch's DOF list
+// is ascending (component, lattice row, lattice column, then the pressure
+// node), so each CSR column is located by binary search.
+std::vector<double> extract_patch(const Level& L, int64_t p) {
+  const int64_t b = L.pstart[p], e = L.pstart[p + 1];
+  const int n = (int)(e - b);
+  const int64_t* dofs = &L.pdof[b];
+  std::vector<double> Ai((size_t)n * n, 0.0);
+  for (int r = 0; r < n; ++r) {
+    const int64_t g = dofs[r];
+    for (int64_t q = L.A.rowptr[g]; q < L.A.rowptr[g + 1]; ++q) {
+      const int64_t* it = std::lower_bound(dofs, dofs + n, (int64_t)L.A.col[q]);
+      if (it != dofs + n && *it == L.A.col[q]) Ai[(size_t)r * n + (it - dofs)] = L.A.val[q];
+    }
+  }
+  return Ai;
+}
+// FNV-1a over the bytes of a matrix (a bucket key only; equality is bitwise)
+uint64_t bytes_hash(const std::vector<double>& a) {
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* s = (const unsigned char*)a.data();
+  for (size_t k = 0; k < a.size() * sizeof(double); ++k) h = (h ^ s[k]) * 1099511628211ull;
+  return h ^ a.size();
+}
+
 bool build_patches(Level& L, double omega, int weighting, std::string& err) {
   const int N = L.N;
   const int64_t nlat = L.nlat, nv = L.nv, npn = L.npn;
@@ -385,45 +411,70 @@ bool build_patches(Level& L, double omega, int weighting, std::string& err) {
       L.pdof.push_back(2 * nv + (int64_t)ky * npn + kx);
       L.pstart[(int64_t)ky * (N + 1) + kx + 1] = (int64_t)L.pdof.size();
     }
-  // extract every A_i, deduplicate by bitwise equality
-  std::map<std::string, int> seen;
+  // extract every A_i, deduplicate by bitwise equality: patch p joins the group
+  // of the first patch (ascending order) whose A_i is bitwise identical, else it
+  // opens a new group.  Only the group representatives are stored; a 64-bit
+  // hash of each A_i's bytes only narrows the candidates -- membership is
+  // decided by a full bitwise comparison with the representative.
   L.pgroup.assign(npatch, -1);
   L.glu.clear();
   L.gpiv.clear();
   L.gsize.clear();
-  std::vector<std::string> keys(npatch);
+  std::vector<uint64_t> hash(npatch);
 #pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t p = 0; p < npatch; ++p) hash[p] = bytes_hash(extract_patch(L, p));
+  std::vector<std::vector<double>> rep;  // A_i of each group's first patch
+  std::multimap<uint64_t, int> by_hash;   // hash -> group ids
+  auto find_group = [&](uint64_t hv, const std::vector<double>& Ai) {
+    auto range = by_hash.equal_range(hv);
+    for (auto it = range.first; it != range.second; ++it)
+      if (rep[it->second].size() == Ai.size() &&
+          std::memcmp(rep[it->second].data(), Ai.data(), Ai.size() * sizeof(double)) == 0)
+        return it->second;
+    return -1;
+  };
+  // pass 1 (serial, ascending patches): a patch whose hash is new opens a group
+  std::vector<uint8_t> settled(npatch, 0);
   for (int64_t p = 0; p < npatch; ++p) {
-    int64_t b = L.pstart[p], e = L.pstart[p + 1];
-    int n = (int)(e - b);
-    std::vector<double> Ai((size_t)n * n, 0.0);
-    for (int r = 0; r < n; ++r) {
-      int64_t g = L.pdof[b + r];
-      for (int64_t q = L.A.rowptr[g]; q < L.A.rowptr[g + 1]; ++q) {
-        int64_t c = L.A.col[q];
-        for (int cc = 0; cc < n; ++cc)
-          if (L.pdof[b + cc] == c) { Ai[(size_t)r * n + cc] = L.A.val[q]; break; }
-      }
-    }
-    std::string key((const char*)&n, sizeof(int));
-    key.append((const char*)Ai.data(), Ai.size() * sizeof(double));
-    keys[p] = std::move(key);
+    if (by_hash.count(hash[p])) continue;
+    std::vector<double> Ai = extract_patch(L, p);
+    int gid = (int)rep.size();
+    rep.push_back(Ai);
+    by_hash.emplace(hash[p], gid);
+    L.pgroup[p] = gid;
+    settled[p] = 1;
   }
+  // pass 2 (parallel): every other patch is compared bitwise with the
+  // representatives of its hash
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t p = 0; p < npatch; ++p)
+    if (!settled[p]) L.pgroup[p] = find_group(hash[p], extract_patch(L, p));
+  // pass 3 (serial): hash collisions without a bitwise match open groups in
+  // ascending patch order (never taken in practice; kept for exactness)
   for (int64_t p = 0; p < npatch; ++p) {
-    auto it = seen.find(keys[p]);
-    if (it != seen.end()) { L.pgroup[p] = it->second; continue; }
-    int n;
-    std::memcpy(&n, keys[p].data(), sizeof(int));
-    std::vector<double> Ai((size_t)n * n);
-    std::memcpy(Ai.data(), keys[p].data() + sizeof(int), Ai.size() * sizeof(double));
+    if (L.pgroup[p] >= 0) continue;
+    std::vector<double> Ai = extract_patch(L, p);
+    int g = find_group(hash[p], Ai);
+    if (g < 0) {
+      g = (int)rep.size();
+      rep.push_back(Ai);
+      by_hash.emplace(hash[p], g);
+    }
+    L.pgroup[p] = g;
+  }
+  // group ids in order of the group's first patch
+  std::vector<int> first(rep.size(), -1), order;
+  for (int64_t p = 0; p < npatch; ++p)
+    if (first[L.pgroup[p]] < 0) { first[L.pgroup[p]] = (int)order.size(); order.push_back(L.pgroup[p]); }
+  for (int64_t p = 0; p < npatch; ++p) L.pgroup[p] = first[L.pgroup[p]];
+  for (int g : order) {
+    std::vector<double> Ai = rep[g];
+    int n = (int)std::lround(std::sqrt((double)Ai.size()));
     std::vector<int> piv;
     if (!lu_factor(Ai, piv, n)) { err = "singular patch matrix"; return false; }
-    int gid = (int)L.glu.size();
     L.glu.push_back(std::move(Ai));
     L.gpiv.push_back(std::move(piv));
     L.gsize.push_back(n);
-    seen.emplace(keys[p], gid);
-    L.pgroup[p] = gid;
   }
   // weights W_i ("the matrix with the weights"; reading 6):
   // multiplicity weighting omega/mult(j), mult(j) = number of patches holding j

@@ -5,7 +5,7 @@
 // nested across levels (r0 doubles from one level to the next finer one).  The
 // coarser levels are replicated: every rank runs them redundantly after an
 // all-gather of the restricted residual.  Vectors keep the full-size pitched
-// layout on every rank; only the owned rows (plus a halo of 3 node rows per
+// layout on every rank; only the owned rows (plus a halo of kHalo = 4 node rows per
 // side, refreshed by `exchange`) are meaningful.
 //
 // Transports:

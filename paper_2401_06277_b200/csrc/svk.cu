@@ -1070,6 +1070,35 @@ int create_impl(svk_ctx* ctx) {
 // =============================================================================
 // C ABI
 // =============================================================================
+// Every entry point that takes a context runs on the context's device (the
+// caller's current device is restored on return) and maps C++ exceptions to
+// status codes, so none crosses the extern "C" boundary.
+template <class F>
+int guarded(svk_ctx* ctx, F&& f) {
+  if (!ctx) return SVK_ERR_INVALID;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != ctx->cfg.device && cudaSetDevice(ctx->cfg.device) != cudaSuccess) {
+    ctx->err = "cudaSetDevice failed";
+    return SVK_ERR_CUDA;
+  }
+  int st;
+  try {
+    st = f();
+  } catch (const std::bad_alloc&) {
+    ctx->err = "host allocation failed";
+    st = SVK_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    ctx->err = std::string("exception: ") + e.what();
+    st = SVK_ERR_INVALID;
+  } catch (...) {
+    ctx->err = "unknown exception";
+    st = SVK_ERR_INVALID;
+  }
+  if (prev >= 0 && prev != ctx->cfg.device) cudaSetDevice(prev);
+  return st;
+}
+
 extern "C" {
 
 int svk_config_default(svk_config* cfg, int32_t n_elem) {
@@ -1130,7 +1159,7 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
     return SVK_ERR_INVALID;
   svk_ctx* ctx = new svk_ctx;
   ctx->cfg = *cfg;
-  int st = create_impl(ctx);
+  int st = guarded(ctx, [&]() -> int { return create_impl(ctx); });
   if (st != SVK_OK) {
     std::fprintf(stderr, "svk_create: %s\n", ctx->err.c_str());
     free_ctx(ctx);
@@ -1142,9 +1171,14 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
 
 int svk_destroy(svk_ctx* ctx) {
   if (!ctx) return SVK_ERR_INVALID;
-  cudaSetDevice(ctx->cfg.device);
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  const int dev = ctx->cfg.device;
+  cudaSetDevice(dev);
   cudaDeviceSynchronize();
-  return free_ctx(ctx);
+  const int st = free_ctx(ctx);
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  return st;
 }
 
 int svk_num_levels(const svk_ctx* ctx, int32_t* levels) {
@@ -1174,187 +1208,221 @@ int svk_level_info(const svk_ctx* ctx, int32_t level, svk_level* out) {
 }
 
 int svk_set_problem(svk_ctx* ctx, int32_t level, int32_t kind, double* b, double* x0, void* stream) {
-  TRY(valid_level(ctx, level));
-  if (kind < 0 || kind > 3) return SVK_ERR_INVALID;
-  if (b) TRY(valid_ptr(ctx, b, "b"));
-  if (x0) TRY(valid_ptr(ctx, x0, "x0"));
-  const LevelGeom& g = ctx->g[level];
-  cudaStream_t s = (cudaStream_t)stream;
-  if (b) CK(cudaMemsetAsync(b, 0, g.len * sizeof(double), s));
-  if (x0) CK(cudaMemsetAsync(x0, 0, g.len * sizeof(double), s));
-  k_set_problem<<<plane_grid(g), kPlaneBlock, 0, s>>>(g, kind, ctx->cfg.nu, b, x0);
-  CKL();
-  return SVK_OK;
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    if (kind < 0 || kind > 3) return SVK_ERR_INVALID;
+    if (b) TRY(valid_ptr(ctx, b, "b"));
+    if (x0) TRY(valid_ptr(ctx, x0, "x0"));
+    const LevelGeom& g = ctx->g[level];
+    cudaStream_t s = (cudaStream_t)stream;
+    if (b) CK(cudaMemsetAsync(b, 0, g.len * sizeof(double), s));
+    if (x0) CK(cudaMemsetAsync(x0, 0, g.len * sizeof(double), s));
+    k_set_problem<<<plane_grid(g), kPlaneBlock, 0, s>>>(g, kind, ctx->cfg.nu, b, x0);
+    CKL();
+    return SVK_OK;
+  });
 }
 
 int svk_residual(svk_ctx* ctx, int32_t level, const double* x, const double* b, double* r, void* stream) {
-  TRY(valid_level(ctx, level));
-  TRY(valid_ptr(ctx, x, "x"));
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, r, "r"));
-  TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
-  return op_residual(ctx, level, x, b, r, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    TRY(valid_ptr(ctx, x, "x"));
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, r, "r"));
+    TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
+    return op_residual(ctx, level, x, b, r, (cudaStream_t)stream);
+  });
 }
 
 int svk_matvec(svk_ctx* ctx, int32_t level, const double* x, double* y, void* stream) {
-  TRY(valid_level(ctx, level));
-  TRY(valid_ptr(ctx, x, "x"));
-  TRY(valid_ptr(ctx, y, "y"));
-  TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
-  return op_residual(ctx, level, x, nullptr, y, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    TRY(valid_ptr(ctx, x, "x"));
+    TRY(valid_ptr(ctx, y, "y"));
+    TRY(op_halo(ctx, level, const_cast<double*>(x), (cudaStream_t)stream));
+    return op_residual(ctx, level, x, nullptr, y, (cudaStream_t)stream);
+  });
 }
 
 int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, int32_t nsweeps,
                     void* stream) {
-  TRY(valid_level(ctx, level));
-  TRY(valid_ptr(ctx, x_in, "x_in"));
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, x_out, "x_out"));
-  if (nsweeps < 1 || x_in == x_out || b == x_out) {
-    ctx->err = "nsweeps < 1 or aliasing x_out";
-    return SVK_ERR_INVALID;
-  }
-  cudaStream_t s = (cudaStream_t)stream;
-  const LevelGeom& g = ctx->g[level];
-  if (ctx->cfg.sweep_impl != SVK_SWEEP_FUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
-  TRY(op_halo(ctx, level, const_cast<double*>(b), s));
-  TRY(op_halo(ctx, level, const_cast<double*>(x_in), s));
-  if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);
-  if (!ctx->d_sw) TRY(alloc_vec(ctx, &ctx->d_sw, ctx->g.back().len));
-  // ping-pong so that the last sweep lands in x_out
-  double* bufs[2] = {x_out, ctx->d_sw};
-  int dst = (nsweeps % 2 == 1) ? 0 : 1;
-  const double* cur = x_in;
-  for (int k = 0; k < nsweeps; ++k) {
-    if (k > 0) TRY(op_halo(ctx, level, const_cast<double*>(cur), s));
-    TRY(op_sweep(ctx, level, cur, b, bufs[dst], false, s));
-    cur = bufs[dst];
-    dst ^= 1;
-  }
-  (void)g;
-  return SVK_OK;
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    TRY(valid_ptr(ctx, x_in, "x_in"));
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, x_out, "x_out"));
+    if (nsweeps < 1 || x_in == x_out || b == x_out) {
+      ctx->err = "nsweeps < 1 or aliasing x_out";
+      return SVK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const LevelGeom& g = ctx->g[level];
+    if (ctx->cfg.sweep_impl != SVK_SWEEP_FUSED && !ctx->d_dbuf) return SVK_ERR_INVALID;
+    TRY(op_halo(ctx, level, const_cast<double*>(b), s));
+    TRY(op_halo(ctx, level, const_cast<double*>(x_in), s));
+    if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);
+    if (!ctx->d_sw) TRY(alloc_vec(ctx, &ctx->d_sw, ctx->g.back().len));
+    // ping-pong so that the last sweep lands in x_out
+    double* bufs[2] = {x_out, ctx->d_sw};
+    int dst = (nsweeps % 2 == 1) ? 0 : 1;
+    const double* cur = x_in;
+    for (int k = 0; k < nsweeps; ++k) {
+      if (k > 0) TRY(op_halo(ctx, level, const_cast<double*>(cur), s));
+      TRY(op_sweep(ctx, level, cur, b, bufs[dst], false, s));
+      cur = bufs[dst];
+      dst ^= 1;
+    }
+    (void)g;
+    return SVK_OK;
+  });
 }
 
 int svk_relax_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const double* b, double* x_out, void* stream) {
-  TRY(valid_level(ctx, level));
-  TRY(valid_ptr(ctx, x_in, "x_in"));
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, x_out, "x_out"));
-  if (x_in == x_out || b == x_out) {
-    ctx->err = "x_out aliases x_in or b";
-    return SVK_ERR_INVALID;
-  }
-  if (ctx->cfg.relax == SVK_RELAX_VANKA) return svk_vanka_sweep(ctx, level, x_in, b, x_out, 1, stream);
-  return op_bs(ctx, level, x_in, b, x_out, false, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    TRY(valid_ptr(ctx, x_in, "x_in"));
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, x_out, "x_out"));
+    if (x_in == x_out || b == x_out) {
+      ctx->err = "x_out aliases x_in or b";
+      return SVK_ERR_INVALID;
+    }
+    if (ctx->cfg.relax == SVK_RELAX_VANKA) return svk_vanka_sweep(ctx, level, x_in, b, x_out, 1, stream);
+    return op_bs(ctx, level, x_in, b, x_out, false, (cudaStream_t)stream);
+  });
 }
 
 int svk_precond_apply(svk_ctx* ctx, const double* b, double* z, void* stream) {
-  if (!ctx) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, z, "z"));
-  if (b == z) {
-    ctx->err = "z aliases b";
-    return SVK_ERR_INVALID;
-  }
-  cudaStream_t s = (cudaStream_t)stream;
-  const int L = ctx->nlev - 1;
-  if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) return op_bt(ctx, b, z, s);
-  TRY(op_halo(ctx, L, const_cast<double*>(b), s));
-  return op_mg(ctx, L, b, z, true, s);
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, z, "z"));
+    if (b == z) {
+      ctx->err = "z aliases b";
+      return SVK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = ctx->nlev - 1;
+    if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) return op_bt(ctx, b, z, s);
+    TRY(op_halo(ctx, L, const_cast<double*>(b), s));
+    return op_mg(ctx, L, b, z, true, s);
+  });
 }
 
 int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream) {
-  TRY(valid_level(ctx, level));
-  if (level < 1) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, r_fine, "r_fine"));
-  TRY(valid_ptr(ctx, r_coarse, "r_coarse"));
-  return op_restrict(ctx, level, r_fine, r_coarse, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    if (level < 1) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, r_fine, "r_fine"));
+    TRY(valid_ptr(ctx, r_coarse, "r_coarse"));
+    return op_restrict(ctx, level, r_fine, r_coarse, (cudaStream_t)stream);
+  });
 }
 
 int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double* x_fine, void* stream) {
-  TRY(valid_level(ctx, level));
-  if (level < 1) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, e_coarse, "e_coarse"));
-  TRY(valid_ptr(ctx, x_fine, "x_fine"));
-  return op_prolong_add(ctx, level, e_coarse, x_fine, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    if (level < 1) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, e_coarse, "e_coarse"));
+    TRY(valid_ptr(ctx, x_fine, "x_fine"));
+    return op_prolong_add(ctx, level, e_coarse, x_fine, (cudaStream_t)stream);
+  });
 }
 
 int svk_coarse_solve(svk_ctx* ctx, const double* b, double* x, void* stream) {
-  if (!ctx) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, x, "x"));
-  return op_coarse(ctx, b, x, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, x, "x"));
+    return op_coarse(ctx, b, x, (cudaStream_t)stream);
+  });
 }
 
 int svk_vcycle(svk_ctx* ctx, const double* b, double* x, void* stream) {
-  if (!ctx) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, x, "x"));
-  if (b == x) return SVK_ERR_INVALID;
-  return op_mg(ctx, ctx->nlev - 1, b, x, false, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, x, "x"));
+    if (b == x) return SVK_ERR_INVALID;
+    return op_mg(ctx, ctx->nlev - 1, b, x, false, (cudaStream_t)stream);
+  });
 }
 
 int svk_fgmres(svk_ctx* ctx, const double* b, double* x, double rtol, int32_t maxit, double* hist, svk_report* rep,
                void* stream) {
-  if (!ctx) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, b, "b"));
-  TRY(valid_ptr(ctx, x, "x"));
-  if (maxit < 1 || !(rtol >= 0) || b == x) return SVK_ERR_INVALID;
-  return fgmres_impl(ctx, b, x, rtol, maxit, hist, rep, (cudaStream_t)stream);
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, x, "x"));
+    if (maxit < 1 || !(rtol >= 0) || b == x) return SVK_ERR_INVALID;
+    return fgmres_impl(ctx, b, x, rtol, maxit, hist, rep, (cudaStream_t)stream);
+  });
 }
 
 int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, double* x_host, double rtol,
                    int32_t maxit, svk_report* rep, void* stream) {
-  if (!ctx || !b_host || !x0_host || !x_host) return SVK_ERR_INVALID;
-  cudaStream_t s = (cudaStream_t)stream;
-  const LevelGeom& g = ctx->g.back();
-  if (!ctx->d_hb) TRY(alloc_vec(ctx, &ctx->d_hb, g.len));
-  if (!ctx->d_hx) TRY(alloc_vec(ctx, &ctx->d_hx, g.len));
-  const int64_t nv = (int64_t)g.lat * g.lat;
-  const size_t wu = g.lat * sizeof(double), wp = (g.N + 1) * sizeof(double);
-  for (int which = 0; which < 2; ++which) {
-    const double* src = which ? x0_host : b_host;
-    double* dst = which ? ctx->d_hx : ctx->d_hb;
-    CK(cudaMemcpy2DAsync(dst + g.oux, g.pu * sizeof(double), src, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpy2DAsync(dst + g.ouy, g.pu * sizeof(double), src + nv, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpy2DAsync(dst + g.op, g.pp * sizeof(double), src + 2 * nv, wp, wp, g.N + 1, cudaMemcpyHostToDevice, s));
-  }
-  int st = fgmres_impl(ctx, ctx->d_hb, ctx->d_hx, rtol, maxit, nullptr, rep, s);
-  if (st < 0) return st;
-  if (ctx->tr) {  // assemble the full solution on every rank
-    TRY(op_zero_unowned(ctx, ctx->nlev - 1, ctx->d_hx, s));
-    TRY(op_allreduce(ctx, ctx->d_hx, g.len, s));
-  }
-  CK(cudaMemcpy2DAsync(x_host, wu, ctx->d_hx + g.oux, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpy2DAsync(x_host + nv, wu, ctx->d_hx + g.ouy, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpy2DAsync(x_host + 2 * nv, wp, ctx->d_hx + g.op, g.pp * sizeof(double), wp, g.N + 1,
-                       cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  return st;
+  return guarded(ctx, [&]() -> int {
+    if (!b_host || !x0_host || !x_host) return SVK_ERR_INVALID;
+    if (maxit < 1 || !(rtol >= 0)) {
+      ctx->err = "maxit < 1 or rtol not >= 0";
+      return SVK_ERR_INVALID;
+    }
+    if (x_host == b_host || x_host == x0_host) {
+      ctx->err = "x_host aliases an input";
+      return SVK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const LevelGeom& g = ctx->g.back();
+    if (!ctx->d_hb) TRY(alloc_vec(ctx, &ctx->d_hb, g.len));
+    if (!ctx->d_hx) TRY(alloc_vec(ctx, &ctx->d_hx, g.len));
+    const int64_t nv = (int64_t)g.lat * g.lat;
+    const size_t wu = g.lat * sizeof(double), wp = (g.N + 1) * sizeof(double);
+    for (int which = 0; which < 2; ++which) {
+      const double* src = which ? x0_host : b_host;
+      double* dst = which ? ctx->d_hx : ctx->d_hb;
+      CK(cudaMemcpy2DAsync(dst + g.oux, g.pu * sizeof(double), src, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpy2DAsync(dst + g.ouy, g.pu * sizeof(double), src + nv, wu, wu, g.lat, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpy2DAsync(dst + g.op, g.pp * sizeof(double), src + 2 * nv, wp, wp, g.N + 1, cudaMemcpyHostToDevice, s));
+    }
+    int st = fgmres_impl(ctx, ctx->d_hb, ctx->d_hx, rtol, maxit, nullptr, rep, s);
+    if (st < 0) return st;
+    if (ctx->tr) {  // assemble the full solution on every rank
+      TRY(op_zero_unowned(ctx, ctx->nlev - 1, ctx->d_hx, s));
+      TRY(op_allreduce(ctx, ctx->d_hx, g.len, s));
+    }
+    CK(cudaMemcpy2DAsync(x_host, wu, ctx->d_hx + g.oux, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(x_host + nv, wu, ctx->d_hx + g.ouy, g.pu * sizeof(double), wu, g.lat, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(x_host + 2 * nv, wp, ctx->d_hx + g.op, g.pp * sizeof(double), wp, g.N + 1,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return st;
+  });
 }
 
 int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y, double* out, int32_t* n) {
-  TRY(valid_level(ctx, level));
-  if (cat_x < 0 || cat_x > 4 || cat_y < 0 || cat_y > 4 || !out || !n) return SVK_ERR_INVALID;
-  const LevelGeom& g = ctx->g[level];
-  std::vector<double> pad(kGroupStride);
-  CK(cudaMemcpy(pad.data(), ctx->d_inv + ((size_t)level * 25 + cat_y * 5 + cat_x) * kGroupStride,
-                kGroupStride * sizeof(double), cudaMemcpyDeviceToHost));
-  const int kx = cat_rep(cat_x, g.N), ky = cat_rep(cat_y, g.N);
-  std::vector<int> slots;
-  for (int comp = 0; comp < 2; ++comp)
-    for (int oy = 0; oy < 5; ++oy)
-      for (int ox = 0; ox < 5; ++ox) {
-        const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
-        if (i < 1 || j < 1 || i > g.lat - 2 || j > g.lat - 2) continue;
-        slots.push_back(comp * 25 + oy * 5 + ox);
-      }
-  slots.push_back(50);
-  const int m = (int)slots.size();
-  for (int r = 0; r < m; ++r)
-    for (int c = 0; c < m; ++c) out[r * m + c] = pad[slots[r] * kSlots + slots[c]];
-  *n = m;
-  return SVK_OK;
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    if (cat_x < 0 || cat_x > 4 || cat_y < 0 || cat_y > 4 || !out || !n) return SVK_ERR_INVALID;
+    const LevelGeom& g = ctx->g[level];
+    std::vector<double> pad(kGroupStride);
+    CK(cudaMemcpy(pad.data(), ctx->d_inv + ((size_t)level * 25 + cat_y * 5 + cat_x) * kGroupStride,
+                  kGroupStride * sizeof(double), cudaMemcpyDeviceToHost));
+    const int kx = cat_rep(cat_x, g.N), ky = cat_rep(cat_y, g.N);
+    std::vector<int> slots;
+    for (int comp = 0; comp < 2; ++comp)
+      for (int oy = 0; oy < 5; ++oy)
+        for (int ox = 0; ox < 5; ++ox) {
+          const int i = 2 * kx - 2 + ox, j = 2 * ky - 2 + oy;
+          if (i < 1 || j < 1 || i > g.lat - 2 || j > g.lat - 2) continue;
+          slots.push_back(comp * 25 + oy * 5 + ox);
+        }
+    slots.push_back(50);
+    const int m = (int)slots.size();
+    for (int r = 0; r < m; ++r)
+      for (int c = 0; c < m; ++c) out[r * m + c] = pad[slots[r] * kSlots + slots[c]];
+    *n = m;
+    return SVK_OK;
+  });
 }
 
 int64_t svk_launch_count(const svk_ctx* ctx) { return ctx ? ctx->launches : -1; }
@@ -1366,18 +1434,20 @@ int svk_set_profiling(svk_ctx* ctx, int32_t enable) {
 }
 
 int svk_sweep_stats(svk_ctx* ctx, int64_t* count, double* total_ms) {
-  if (!ctx || !count || !total_ms) return SVK_ERR_INVALID;
-  CK(cudaDeviceSynchronize());
-  double t = 0.0;
-  for (size_t k = 0; k + 1 < ctx->prof_used; k += 2) {
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, ctx->prof_ev[k], ctx->prof_ev[k + 1]));
-    t += ms;
-  }
-  *count = (int64_t)(ctx->prof_used / 2);
-  *total_ms = t;
-  ctx->prof_used = 0;
-  return SVK_OK;
+  return guarded(ctx, [&]() -> int {
+    if (!ctx || !count || !total_ms) return SVK_ERR_INVALID;
+    CK(cudaDeviceSynchronize());
+    double t = 0.0;
+    for (size_t k = 0; k + 1 < ctx->prof_used; k += 2) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->prof_ev[k], ctx->prof_ev[k + 1]));
+      t += ms;
+    }
+    *count = (int64_t)(ctx->prof_used / 2);
+    *total_ms = t;
+    ctx->prof_used = 0;
+    return SVK_OK;
+  });
 }
 
 int svk_partition(int32_t n_elem, int32_t n_coarse, int32_t nranks, int32_t rank, int32_t agglom_rows, int32_t N,
@@ -1415,12 +1485,14 @@ int svk_nccl_unique_id(uint8_t* out) {
 }
 
 int svk_allgather(svk_ctx* ctx, double* v, void* stream) {
-  if (!ctx) return SVK_ERR_INVALID;
-  TRY(valid_ptr(ctx, v, "v"));
-  if (!ctx->tr) return SVK_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  TRY(op_zero_unowned(ctx, ctx->nlev - 1, v, s));
-  return op_allreduce(ctx, v, ctx->g.back().len, s);
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, v, "v"));
+    if (!ctx->tr) return SVK_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(op_zero_unowned(ctx, ctx->nlev - 1, v, s));
+    return op_allreduce(ctx, v, ctx->g.back().len, s);
+  });
 }
 
 const char* svk_status_string(int status) {

@@ -144,10 +144,6 @@ def nccl_id_broadcast(group=None, make_id=None) -> bytes:
     return bytes(obj[0])
 
 
-def _stream(torch):
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
-
-
 class Solver:
     """One libsvk context: hierarchy N, N/2, ..., n_coarse on one CUDA device."""
 
@@ -225,14 +221,21 @@ class Solver:
             raise SvkError("%s: %s" % (self.lib.svk_status_string(st).decode(), msg.decode() if msg else ""))
         return st
 
+    def _stream(self):
+        """This context's device's current torch stream (the library itself runs
+        every call on cfg.device and restores the caller's device)."""
+        return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
     @property
     def fine(self) -> int:
         return self.levels - 1
 
     def _vec(self, t, level, name):
         li = self.info[level]
-        if t.dtype != self.torch.float64 or not t.is_cuda or not t.is_contiguous() or t.numel() != li.vec_len:
-            raise SvkError("%s: expected a contiguous float64 CUDA tensor of %d elements" % (name, li.vec_len))
+        if (t.dtype != self.torch.float64 or not t.is_cuda or t.device != self.device or not t.is_contiguous()
+                or t.numel() != li.vec_len):
+            raise SvkError("%s: expected a contiguous float64 tensor of %d elements on %s"
+                           % (name, li.vec_len, self.device))
         return C.c_void_p(t.data_ptr())
 
     def new_vector(self, level: int | None = None):
@@ -271,62 +274,62 @@ class Solver:
         level = self.fine if level is None else level
         b, x0 = self.new_vector(level), self.new_vector(level)
         self._chk(self.lib.svk_set_problem(self._h, level, PROBLEMS[kind], C.c_void_p(b.data_ptr()),
-                                           C.c_void_p(x0.data_ptr()), _stream(self.torch)))
+                                           C.c_void_p(x0.data_ptr()), self._stream()))
         return b, x0
 
     def residual(self, level, x, b, out=None):
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_residual(self._h, level, self._vec(x, level, "x"), self._vec(b, level, "b"),
-                                        self._vec(out, level, "r"), _stream(self.torch)))
+                                        self._vec(out, level, "r"), self._stream()))
         return out
 
     def matvec(self, level, x, out=None):
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_matvec(self._h, level, self._vec(x, level, "x"), self._vec(out, level, "y"),
-                                      _stream(self.torch)))
+                                      self._stream()))
         return out
 
     def sweep(self, level, x, b, nsweeps: int = 1, out=None):
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_vanka_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
-                                           self._vec(out, level, "x_out"), nsweeps, _stream(self.torch)))
+                                           self._vec(out, level, "x_out"), nsweeps, self._stream()))
         return out
 
     def relax_sweep(self, level, x, b, out=None):
         """One sweep of the configured relaxation (svk_relax_sweep)."""
         out = self.new_vector(level) if out is None else out
         self._chk(self.lib.svk_relax_sweep(self._h, level, self._vec(x, level, "x_in"), self._vec(b, level, "b"),
-                                           self._vec(out, level, "x_out"), _stream(self.torch)))
+                                           self._vec(out, level, "x_out"), self._stream()))
         return out
 
     def precond_apply(self, b, out=None):
         """z = M b with the configured FGMRES preconditioner (svk_precond_apply)."""
         out = self.new_vector() if out is None else out
         self._chk(self.lib.svk_precond_apply(self._h, self._vec(b, self.fine, "b"), self._vec(out, self.fine, "z"),
-                                             _stream(self.torch)))
+                                             self._stream()))
         return out
 
     def restrict(self, level, rf, out=None):
         out = self.new_vector(level - 1) if out is None else out
         self._chk(self.lib.svk_restrict(self._h, level, self._vec(rf, level, "r_fine"),
-                                        self._vec(out, level - 1, "r_coarse"), _stream(self.torch)))
+                                        self._vec(out, level - 1, "r_coarse"), self._stream()))
         return out
 
     def prolong_add(self, level, ec, xf):
         self._chk(self.lib.svk_prolong_add(self._h, level, self._vec(ec, level - 1, "e_coarse"),
-                                           self._vec(xf, level, "x_fine"), _stream(self.torch)))
+                                           self._vec(xf, level, "x_fine"), self._stream()))
         return xf
 
     def coarse_solve(self, b, out=None):
         out = self.new_vector(0) if out is None else out
         self._chk(self.lib.svk_coarse_solve(self._h, self._vec(b, 0, "b"), self._vec(out, 0, "x"),
-                                            _stream(self.torch)))
+                                            self._stream()))
         return out
 
     def vcycle(self, b, x=None):
         x = self.new_vector() if x is None else x
         self._chk(self.lib.svk_vcycle(self._h, self._vec(b, self.fine, "b"), self._vec(x, self.fine, "x"),
-                                      _stream(self.torch)))
+                                      self._stream()))
         return x
 
     def fgmres(self, b, x, rtol: float = 1e-10, maxit: int = 200):
@@ -335,7 +338,7 @@ class Solver:
         rep = Report()
         st = self._chk(self.lib.svk_fgmres(self._h, self._vec(b, self.fine, "b"), self._vec(x, self.fine, "x"),
                                            rtol, maxit, hist.ctypes.data_as(C.c_void_p), C.byref(rep),
-                                           _stream(self.torch)))
+                                           self._stream()))
         d = rep.as_dict()
         d["status"] = st
         return d, hist[: rep.iterations + 1].copy()
@@ -343,20 +346,31 @@ class Solver:
     def solve_host(self, b_host: np.ndarray, x0_host: np.ndarray, rtol: float = 1e-10, maxit: int = 200,
                    x_host: np.ndarray | None = None):
         """End-to-end solve from host arrays in the compact layout (svk_solve_host)."""
-        b_host = np.ascontiguousarray(b_host, dtype=np.float64)
-        x0_host = np.ascontiguousarray(x0_host, dtype=np.float64)
-        x_host = np.empty_like(b_host) if x_host is None else x_host
+        li = self.info[self.fine]
+        n = 2 * li.lat * li.lat + (li.N + 1) ** 2
+
+        def host(a, name, writable=False):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+                    and a.ndim == 1 and a.size == n and (a.flags["WRITEABLE"] or not writable)):
+                raise SvkError("%s: expected a C-contiguous%s float64 host array of %d elements"
+                               % (name, " writable" if writable else "", n))
+            return a
+
+        b_host, x0_host = host(b_host, "b_host"), host(x0_host, "x0_host")
+        x_host = np.empty_like(b_host) if x_host is None else host(x_host, "x_host", writable=True)
+        if np.shares_memory(x_host, b_host) or np.shares_memory(x_host, x0_host):
+            raise SvkError("x_host aliases an input")
         rep = Report()
         st = self._chk(self.lib.svk_solve_host(self._h, b_host.ctypes.data_as(C.c_void_p),
                                                x0_host.ctypes.data_as(C.c_void_p), x_host.ctypes.data_as(C.c_void_p),
-                                               rtol, maxit, C.byref(rep), _stream(self.torch)))
+                                               rtol, maxit, C.byref(rep), self._stream()))
         d = rep.as_dict()
         d["status"] = st
         return x_host, d
 
     def allgather(self, v):
         """Distributed mode: complete every rank's copy of a finest-level vector (in place)."""
-        self._chk(self.lib.svk_allgather(self._h, self._vec(v, self.fine, "v"), _stream(self.torch)))
+        self._chk(self.lib.svk_allgather(self._h, self._vec(v, self.fine, "v"), self._stream()))
         return v
 
     def owned_rows(self, level: int | None = None):

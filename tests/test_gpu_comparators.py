@@ -6,6 +6,7 @@ correction per sweep / V-cycle, FGMRES iterations within +-1.  Sizes span every
 level of the hierarchy (N = 4 ... 256), i.e. the tiny-level S classes, the seven
 boundary-distance classes per axis and ragged CUDA blocks."""
 import numpy as np
+from parity_util import rel
 import pytest
 
 import oracle
@@ -17,8 +18,6 @@ KINDS = {"bs": (oracle.RELAX_BS, dict(t=1.0, omega_r=1.0, omega_j=0.8, nj=3)),
          "su": (oracle.RELAX_SU, dict(t=1.0, omega_j=0.4, nj=1))}
 
 
-def rel(a, b):
-    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
 def make(N, kind, **over):

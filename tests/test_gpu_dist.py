@@ -10,6 +10,7 @@ import itertools
 import threading
 
 import numpy as np
+from parity_util import rel
 import pytest
 
 import oracle
@@ -20,9 +21,6 @@ pytestmark = pytest.mark.gpu
 _group = itertools.count(1000)
 
 
-def rel(a, b):
-    a, b = np.asarray(a), np.asarray(b)
-    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
 def run_ranks(P, fn, timeout=300):

@@ -3,6 +3,7 @@ patch factors scale with it: L = nu (M (x) K + K (x) M)), V(2,2) cycle
 (alg:mg nu1 = nu2 = 2) and another Vanka weight, each against the oracle
 built with the same parameters.  1e-12 relative as everywhere (north_star)."""
 import numpy as np
+from parity_util import rel
 import pytest
 
 import oracle
@@ -11,8 +12,6 @@ import svk_inputs
 pytestmark = pytest.mark.gpu
 
 
-def rel(a, b):
-    return float(np.linalg.norm(np.asarray(a) - b) / max(np.linalg.norm(b), 1e-300))
 
 
 @pytest.mark.parametrize("nu", [0.01, 7.5])

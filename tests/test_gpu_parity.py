@@ -5,6 +5,7 @@ FGMRES iteration counts within +-1.  Sizes span several tiles and ragged tails
 (N+1 = 17, 65, 129, 257 node columns vs the kernels' strip widths).
 """
 import numpy as np
+from parity_util import rel
 import pytest
 
 import oracle
@@ -15,9 +16,6 @@ pytestmark = pytest.mark.gpu
 IMPLS = ["fused", "unfused", "simple"]  # simple: per-patch stored inverses (NEXT-3)
 
 
-def rel(a, b):
-    a, b = np.asarray(a), np.asarray(b)
-    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
 _orc = {}
@@ -257,3 +255,34 @@ def test_errors_are_loud(gpu):
         S.residual(S.fine, x[:-1].clone(), x)        # wrong length
     with pytest.raises(SvkError):
         S.restrict(0, S.new_vector(0))               # no coarser level
+
+
+def test_host_arrays_and_arguments_are_checked(gpu):
+    """svk_solve_host reads / writes 2(2N+1)^2+(N+1)^2 doubles: the binding rejects
+    short, wrongly typed, non-contiguous or read-only arrays, and the C entry point
+    itself rejects maxit < 1, a NaN rtol and an aliased output."""
+    import ctypes as C
+    from paper_2401_06277_b200 import SvkError
+    from paper_2401_06277_b200.svk import Report
+    N = 16
+    S = get_solver(N)
+    n = 2 * (2 * N + 1) ** 2 + (N + 1) ** 2
+    ok = np.zeros(n)
+    for bad in (np.zeros(n - 1), np.zeros(n, np.float32), np.zeros(2 * n)[::2]):
+        with pytest.raises(SvkError):
+            S.solve_host(bad, ok)
+        with pytest.raises(SvkError):
+            S.solve_host(ok, bad)
+    ro = np.zeros(n)
+    ro.flags.writeable = False
+    with pytest.raises(SvkError):
+        S.solve_host(ok, ok, x_host=ro)
+    with pytest.raises(SvkError):
+        S.solve_host(ok, ok.copy(), x_host=ok)
+    p = ok.ctypes.data_as(C.c_void_p)
+    out = np.zeros(n)
+    q = out.ctypes.data_as(C.c_void_p)
+    rep = Report()
+    for rtol, maxit in ((1e-10, 0), (1e-10, -5), (float("nan"), 10), (-1.0, 10)):
+        assert S.lib.svk_solve_host(S._h, p, p, q, rtol, maxit, C.byref(rep), None) < 0
+    assert S.lib.svk_solve_host(S._h, p, p, p, 1e-10, 10, C.byref(rep), None) < 0
