@@ -72,6 +72,24 @@ struct svk_ctx {
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;  // pool, used in (start, stop) pairs
   size_t prof_used = 0;
+  // CUDA graphs of the FGMRES preconditioner (one V-cycle from zero, alg:mg),
+  // captured once per (input, output) basis-vector pair and replayed: the ~60
+  // kernels of a cycle become one graph launch (programmatic edges kept).
+  struct GraphRec {
+    const double* in = nullptr;
+    double* out = nullptr;
+    bool prof = false;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;                                   // kernels in the graph
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // timed finest-level sweeps
+  };
+  std::vector<std::unique_ptr<GraphRec>> graphs;
+  GraphRec* capturing = nullptr;
+  std::vector<GraphRec*> prof_pending;  // replayed graphs whose sweep events are not harvested yet
+  cudaStream_t cap_stream = nullptr;
+  int use_graphs = -1;                  // -1: decide at first use (SVK_GRAPHS=0 disables)
+  double prof_acc_ms = 0.0;
+  int64_t prof_acc_n = 0;
   // multi-GPU row slabs (dist.cuh): levels la..nlev-1 are distributed
   std::unique_ptr<Transport> tr;
   int la = 1 << 30;
@@ -370,6 +388,16 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
 int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero, cudaStream_t s) {
   // only full sweeps (non-zero x_in) are timed, so the roofline's per-unit counts apply
   const bool timed = ctx->prof && l == ctx->nlev - 1 && !x_zero;
+  if (timed && ctx->capturing) {  // events owned by the graph being captured
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    ctx->capturing->ev.emplace_back(e0, e1);
+    CK(cudaEventRecord(e0, s));
+    TRY(op_sweep_impl(ctx, l, xin, b, xout, x_zero, s));
+    CK(cudaEventRecord(e1, s));
+    return SVK_OK;
+  }
   if (timed) {
     while (ctx->prof_ev.size() < ctx->prof_used + 2) {
       cudaEvent_t e;
@@ -615,6 +643,71 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
   return SVK_OK;
 }
 
+// Sweep times of replayed graphs (their events are re-recorded at every replay,
+// so each replay is harvested after the stream synchronisation that follows it).
+int harvest_graph_prof(svk_ctx* ctx) {
+  for (auto* gr : ctx->prof_pending)
+    for (auto& pr : gr->ev) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      ctx->prof_acc_ms += ms;
+      ctx->prof_acc_n++;
+    }
+  ctx->prof_pending.clear();
+  return SVK_OK;
+}
+
+// z = M v (one V-cycle from zero on the finest level) for FGMRES: replayed from a
+// CUDA graph captured on the library's own stream at the first use of the pair
+// (v, z); single-GPU contexts only (the emulated transport synchronises host
+// threads inside a cycle, which a graph cannot hold).  Falls back to direct
+// launches if capture is unavailable.
+int op_precond_mg(svk_ctx* ctx, const double* v, double* z, cudaStream_t s) {
+  const int L = ctx->nlev - 1;
+  if (ctx->use_graphs < 0) {
+    const char* e = std::getenv("SVK_GRAPHS");
+    ctx->use_graphs = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!ctx->use_graphs || ctx->tr) return op_mg(ctx, L, v, z, true, s);
+  svk_ctx::GraphRec* gr = nullptr;
+  for (auto& g : ctx->graphs)
+    if (g->in == v && g->out == z && g->prof == ctx->prof) gr = g.get();
+  if (!gr) {
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    auto rec = std::make_unique<svk_ctx::GraphRec>();
+    rec->in = v;
+    rec->out = z;
+    rec->prof = ctx->prof;
+    const int64_t l0 = ctx->launches;
+    ctx->capturing = rec.get();
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+    const int st = op_mg(ctx, L, v, z, true, ctx->cap_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    ctx->capturing = nullptr;
+    rec->launches = ctx->launches - l0;
+    ctx->launches = l0;
+    cudaError_t ie = cudaErrorUnknown;
+    if (st == SVK_OK && ce == cudaSuccess && graph) ie = cudaGraphInstantiate(&rec->exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {  // no graph: direct launches from now on
+      cudaGetLastError();
+      for (auto& pr : rec->ev) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+      ctx->use_graphs = 0;
+      return op_mg(ctx, L, v, z, true, s);
+    }
+    gr = rec.get();
+    ctx->graphs.push_back(std::move(rec));
+  }
+  CK(cudaGraphLaunch(gr->exec, s));
+  ctx->launches += gr->launches;
+  if (gr->prof && !gr->ev.empty()) ctx->prof_pending.push_back(gr);
+  return SVK_OK;
+}
+
 int ensure_coef(svk_ctx* ctx, int need) {
   if (need <= ctx->coef_cap) return SVK_OK;
   int cap = std::max(need, 2 * ctx->coef_cap);
@@ -739,7 +832,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       // z~_j = M V~_j : one V-cycle from zero
       CK(cudaEventRecord(ctx->ev[0], s));
       if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) TRY(op_bt(ctx, ctx->V[j], ctx->Z[j], s));
-      else TRY(op_mg(ctx, L, ctx->V[j], ctx->Z[j], true, s));
+      else TRY(op_precond_mg(ctx, ctx->V[j], ctx->Z[j], s));
       CK(cudaEventRecord(ctx->ev[1], s));
       // w~ = A z~_j ; classical Gram-Schmidt pass against V~_0..V~_j (its dot
       // pass also yields |w~|^2) ; V~_j+1 = w~' with |w~'|
@@ -753,6 +846,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       CK(cudaEventRecord(ctx->ev[2], s));
       CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      TRY(harvest_graph_prof(ctx));
       float a01 = 0, a12 = 0;
       cudaEventElapsedTime(&a01, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&a12, ctx->ev[1], ctx->ev[2]);
@@ -879,6 +973,14 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_hx);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   for (auto e : ctx->prof_ev) cudaEventDestroy(e);
+  for (auto& gr : ctx->graphs) {
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    for (auto& pr : gr->ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  }
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   delete ctx;
@@ -1443,9 +1545,12 @@ int svk_sweep_stats(svk_ctx* ctx, int64_t* count, double* total_ms) {
       CK(cudaEventElapsedTime(&ms, ctx->prof_ev[k], ctx->prof_ev[k + 1]));
       t += ms;
     }
-    *count = (int64_t)(ctx->prof_used / 2);
-    *total_ms = t;
+    TRY(harvest_graph_prof(ctx));
+    *count = (int64_t)(ctx->prof_used / 2) + ctx->prof_acc_n;
+    *total_ms = t + ctx->prof_acc_ms;
     ctx->prof_used = 0;
+    ctx->prof_acc_n = 0;
+    ctx->prof_acc_ms = 0.0;
     return SVK_OK;
   });
 }

@@ -43,7 +43,8 @@ def run(env_extra, N):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("env_extra", [{"SVK_PDL": "0"}, {"SVK_CHUNK_ROWS": "8"}, {"SVK_CHUNK_ROWS": "1000"}])
+@pytest.mark.parametrize("env_extra", [{"SVK_PDL": "0"}, {"SVK_CHUNK_ROWS": "8"}, {"SVK_CHUNK_ROWS": "1000"},
+                                       {"SVK_GRAPHS": "0"}])
 def test_launch_switches_keep_parity(gpu, env_extra):
     N = 128
     r = run(env_extra, N)
@@ -54,3 +55,45 @@ def test_launch_switches_keep_parity(gpu, env_extra):
     bo, x0o = O.problem(oracle.MMS_PAPER)
     its_o = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)[1]
     assert abs(r["its"] - its_o) <= 1, (r, its_o)
+
+
+GRAPH_SCRIPT = r"""
+import json, sys
+import numpy as np
+import torch
+from paper_2401_06277_b200 import Solver
+N = int(sys.argv[1])
+S = Solver(N)
+b, x0 = S.set_problem("mms_paper")
+S.set_profiling(True)
+S.sweep_stats()
+out = []
+for rep_i in range(2):  # the second solve replays the captured graphs
+    x = x0.clone()
+    l0 = S.launch_count
+    rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=100)
+    torch.cuda.synchronize()
+    nsw, ms = S.sweep_stats()
+    out.append({"its": rep["iterations"], "hist": hist.tolist(), "x": float(x.double().abs().sum()),
+                "xhash": float((x * torch.arange(x.numel(), device=x.device, dtype=x.dtype).remainder(97)).sum()),
+                "launches": S.launch_count - l0, "nsw": nsw, "sweep_ms": ms})
+print(json.dumps(out))
+"""
+
+
+def test_graph_replay_is_bitwise_identical_to_direct_launches(gpu):
+    """The FGMRES preconditioner V-cycle replayed from captured CUDA graphs gives
+    bitwise the same iterates as direct launches (fixed reduction orders), and
+    the graph path still reports its kernel count and the timed finest sweeps."""
+    res = {}
+    for g in ("0", "1"):
+        env = dict(os.environ, PYTHONPATH=ROOT, SVK_GRAPHS=g)
+        out = subprocess.run([sys.executable, "-c", GRAPH_SCRIPT, "256"], cwd=ROOT, env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[g] = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in range(2):
+        a, c = res["0"][k], res["1"][k]
+        assert a["its"] == c["its"] and a["hist"] == c["hist"] and a["x"] == c["x"] and a["xhash"] == c["xhash"]
+        assert a["launches"] == c["launches"] > 0
+        assert a["nsw"] == c["nsw"] == a["its"] and c["sweep_ms"] > 0

@@ -7,10 +7,10 @@ S=/usr/local/cuda/bin/compute-sanitizer
 for N in 64 256; do
   for tool in memcheck racecheck synccheck initcheck; do
     extra=""
-    [ $tool = racecheck ] && extra="--racecheck-report all"
-    [ $tool = initcheck ] && extra="--track-unused-memory no"
+    [ $tool = racecheck ] && extra="--racecheck-report hazard"
+    true
     log=gpurun_out/sanitizer_${tool}_${N}.log
-    timeout 900 $S --tool $tool $extra --print-limit 50 python tools/sanitize_driver.py $N > $log 2>&1
+    PYTHONPATH=. timeout 900 $S --tool $tool $extra --print-limit 50 python tools/sanitize_driver.py $N > $log 2>&1
     rc=$?
     echo "N=$N tool=$tool rc=$rc :: $(grep -E '^ok|ERROR SUMMARY|RACECHECK SUMMARY|hazard' $log | tail -3 | tr '\n' ' ')" >> gpurun_out/sanitizer_summary.txt
   done
