@@ -42,7 +42,8 @@
  * SVK_ERR_INVALID: bad level / size / NULL or misaligned pointer;
  * SVK_ERR_CUDA: a CUDA runtime error (the context may be unusable afterwards);
  * SVK_ERR_SINGULAR: a patch or coarse factorisation met a zero pivot;
- * SVK_ERR_NONFINITE: FGMRES met NaN/Inf.
+ * SVK_ERR_NONFINITE: FGMRES met NaN/Inf;
+ * SVK_ERR_VALIDATION: validation mode found a patch that differs from its group.
  *
  * THREADING.  One context per device; calls on one context must not overlap
  * (scratch is per context).  Different contexts are independent: every call
@@ -87,7 +88,8 @@ enum svk_status {
   SVK_ERR_NCCL = -3,
   SVK_ERR_SINGULAR = -4,
   SVK_ERR_NONFINITE = -5,
-  SVK_ERR_ALLOC = -6
+  SVK_ERR_ALLOC = -6,
+  SVK_ERR_VALIDATION = -7
 };
 
 /* W_i of alg:vk ("the matrix with the weights"; unstated in the paper):
@@ -149,7 +151,9 @@ typedef struct svk_config {
   int32_t precond;       /* enum svk_precond: FGMRES preconditioner; default MG */
   int32_t bt_cycles;     /* BLOCK_TRIANGULAR: V-cycles per block; default 3 */
   int32_t bt_nu;         /* BLOCK_TRIANGULAR: Jacobi sweeps before / after; default 3 (V(3,3)) */
-  int32_t bt_reserved;
+  int32_t validate;      /* validation mode ("only 25 different patch matrices"):
+                            svk_create rebuilds every patch of every level on its own and
+                            checks it against its group (svk_validate_patches); default 0 */
   double bt_omega_u;     /* BLOCK_TRIANGULAR: Jacobi weight on L; default 1.0 */
   double bt_omega_p;     /* BLOCK_TRIANGULAR: Jacobi weight on M; default 0.6 */
 } svk_config;
@@ -306,6 +310,17 @@ int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y,
 
 /* Number of kernel launches issued by this context since creation (for the
  * benchmark's gpu_launches count). */
+/* Validation mode.  Every patch of `level` is
+ * rebuilt from the stencil on its own (A_i = V_i A V_i^T) and inverted
+ * (batched fp64 Gauss-Jordan), and compared with the stored inverse of its
+ * group; the generic group's reflection-basis Schur factors (the fused sweep's
+ * solve) are applied to the 51 unit vectors and compared with the generic
+ * group's inverse.  *max_rel_dev (host, optional) = max |a - b| / max |group
+ * inverse| over all of them, *n_patches = (N+1)^2.  Synchronous.  Returns
+ * SVK_OK if max_rel_dev <= 1e-12, else SVK_ERR_VALIDATION (message names the
+ * deviation); workspace ~170 MB, freed on return. */
+int svk_validate_patches(svk_ctx* ctx, int32_t level, double* max_rel_dev, int64_t* n_patches);
+
 int64_t svk_launch_count(const svk_ctx* ctx);
 
 /* Benchmark support.  While profiling is enabled, every full Vanka sweep (non-

@@ -465,8 +465,11 @@ __global__ void k_patch_setup(const int* __restrict__ Ns, double nu, double* __r
 // the patches, inv[(r * 51 + c) * np + p], so that the apply kernel's per-patch
 // reads are coalesced across the threads of a warp.
 // ---------------------------------------------------------------------------
+// (stride, base): entry q of patch p is stored at inv_out[q * stride + p - base]
+// (the simple-Vanka store uses stride = patch count, base = 0; the validation
+// mode builds batches of `stride` patches starting at base).
 __global__ void k_patch_setup_simple(LevelGeom g, double nu, int64_t p0, double* __restrict__ inv_out,
-                                     int* __restrict__ status) {
+                                     int* __restrict__ status, int64_t stride, int64_t base) {
   const int N = g.N, lat = g.lat;
   const int64_t np = (int64_t)(N + 1) * (N + 1);
   const int64_t p = p0 + blockIdx.x;
@@ -498,14 +501,14 @@ __global__ void k_patch_setup_simple(LevelGeom g, double nu, int64_t p0, double*
   for (int q = threadIdx.x; q < nn * nn; q += blockDim.x) a[q] = a_entry(dof[q / nn], dof[q % nn], N, nu, g.h);
   __syncthreads();
   const bool ok = gj_invert(a, nn, nn, perm, colk, &flag);
-  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) inv_out[(int64_t)q * np + p] = 0.0;
+  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) inv_out[(int64_t)q * stride + p - base] = 0.0;
   __syncthreads();
   if (!ok) {
     if (threadIdx.x == 0) atomicExch(status, 1);
     return;
   }
   for (int q = threadIdx.x; q < nn * nn; q += blockDim.x)
-    inv_out[(int64_t)(slot[q / nn] * kSlots + slot[q % nn]) * np + p] = a[q];
+    inv_out[(int64_t)(slot[q / nn] * kSlots + slot[q % nn]) * stride + p - base] = a[q];
 }
 // delta_p = A_p^{-1} V_p r with patch p's own stored inverse (one thread per patch)
 __global__ void __launch_bounds__(128) k_patch_solve_simple(LevelGeom g, const double* __restrict__ r,

@@ -393,9 +393,11 @@ int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     ctx->capturing->ev.emplace_back(e0, e1);
-    CK(cudaEventRecord(e0, s));
+    // cudaEventRecordExternal: real event-record nodes in the captured graph
+    // (a plain record during capture only expresses a dependency)
+    CK(cudaEventRecordWithFlags(e0, s, cudaEventRecordExternal));
     TRY(op_sweep_impl(ctx, l, xin, b, xout, x_zero, s));
-    CK(cudaEventRecord(e1, s));
+    CK(cudaEventRecordWithFlags(e1, s, cudaEventRecordExternal));
     return SVK_OK;
   }
   if (timed) {
@@ -643,6 +645,63 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
   return SVK_OK;
 }
 
+// Validation mode (see k_validate_batch): max relative deviation on level l of
+// (a) every patch's own inverse from its group's stored inverse, (b) the generic
+// reflection-basis factors from the generic group's inverse.
+int op_validate(svk_ctx* ctx, int l, double* max_dev, int64_t* n_patch) {
+  const LevelGeom& g = ctx->g[l];
+  const int64_t np = (int64_t)(g.N + 1) * (g.N + 1);
+  std::vector<double> ginv((size_t)25 * kGroupStride), scale(25, 0.0);
+  const double* dg = ctx->d_inv + (size_t)l * 25 * kGroupStride;
+  CK(cudaMemcpy(ginv.data(), dg, ginv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 25; ++k)
+    for (int q = 0; q < kGroupStride; ++q) scale[k] = std::max(scale[k], std::fabs(ginv[(size_t)k * kGroupStride + q]));
+  const int64_t nb = std::min<int64_t>(np, 8192);
+  double *d_batch = nullptr, *d_scale = nullptr, *d_dev = nullptr;
+  int* d_st = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(d_batch);
+    cudaFree(d_scale);
+    cudaFree(d_dev);
+    cudaFree(d_st);
+  };
+  if (cudaMalloc(&d_batch, (size_t)nb * kGroupStride * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d_scale, 25 * sizeof(double)) != cudaSuccess || cudaMalloc(&d_dev, 2 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&d_st, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    ctx->err = "validation: workspace allocation failed";
+    return SVK_ERR_ALLOC;
+  }
+  cudaMemcpy(d_scale, scale.data(), 25 * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemset(d_dev, 0, 2 * sizeof(double));
+  cudaMemset(d_st, 0, sizeof(int));
+  for (int64_t p0 = 0; p0 < np; p0 += nb) {
+    const int64_t n = std::min(nb, np - p0);
+    k_patch_setup_simple<<<(unsigned)n, 128>>>(g, ctx->cfg.nu, p0, d_batch, d_st, nb, p0);
+    k_validate_batch<<<(unsigned)std::min<int64_t>((n * kGroupStride + 255) / 256, 4096), 256>>>(
+        g, p0, nb, d_batch, dg, d_scale, d_dev);
+  }
+  k_validate_factors<<<1, 64>>>(ctx->h_fac[l], dg + (size_t)12 * kGroupStride, scale[12], d_dev + 1);
+  double dev[2] = {0, 0};
+  int st = 0;
+  const cudaError_t e1 = cudaMemcpy(dev, d_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+  const cudaError_t e2 = cudaMemcpy(&st, d_st, sizeof(int), cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    ctx->err = std::string("validation: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
+    return SVK_ERR_CUDA;
+  }
+  if (st) {
+    ctx->err = "validation: singular patch matrix";
+    return SVK_ERR_SINGULAR;
+  }
+  *max_dev = std::max(dev[0], g.N >= 4 ? dev[1] : 0.0);
+  *n_patch = np;
+  return SVK_OK;
+}
+constexpr double kValidateTol = 1e-12;
+
 // Sweep times of replayed graphs (their events are re-recorded at every replay,
 // so each replay is harvested after the stream synchronisation that follows it).
 int harvest_graph_prof(svk_ctx* ctx) {
@@ -714,7 +773,9 @@ int ensure_coef(svk_ctx* ctx, int need) {
   if (ctx->d_coef) cudaFree(ctx->d_coef);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   CK(cudaMalloc(&ctx->d_coef, cap * sizeof(double)));
+  CK(cudaMemset(ctx->d_coef, 0, cap * sizeof(double)));  // read back in whole blocks: keep it defined
   CK(cudaMallocHost(&ctx->h_pin, cap * sizeof(double)));
+  std::memset(ctx->h_pin, 0, cap * sizeof(double));
   ctx->coef_cap = cap;
   return SVK_OK;
 }
@@ -1039,6 +1100,17 @@ int create_impl(svk_ctx* ctx) {
   CK(cudaMalloc(&ctx->d_fac, (size_t)ctx->nlev * kFacStride * sizeof(double)));
   TRY(launch_factor_setup(ctx->d_Ns, ctx->nlev, c.nu, ctx->d_inv, ctx->d_fac, d_status));
   CKL();
+  if (const char* cg = std::getenv("SVK_TEST_CORRUPT_GROUP")) {  // test aid: "level,group,slot"
+    int cl = -1, cgp = -1, cq = -1;
+    if (std::sscanf(cg, "%d,%d,%d", &cl, &cgp, &cq) == 3 && cl >= 0 && cl < ctx->nlev && cgp >= 0 && cgp < 25 &&
+        cq >= 0 && cq < kGroupStride) {
+      double* e = ctx->d_inv + ((size_t)cl * 25 + cgp) * kGroupStride + cq;
+      double v;
+      CK(cudaMemcpy(&v, e, sizeof(double), cudaMemcpyDeviceToHost));
+      v = v * (1.0 + 1e-9) + 1e-12;
+      CK(cudaMemcpy(e, &v, sizeof(double), cudaMemcpyHostToDevice));
+    }
+  }
   // level-0 bordered pseudo-inverse
   const LevelGeom& g0 = ctx->g[0];
   std::vector<int> idx;
@@ -1110,7 +1182,8 @@ int create_impl(svk_ctx* ctx) {
       }
       ctx->d_inv_simple.push_back(p);
       for (int64_t p0 = 0; p0 < np; p0 += (1 << 30))
-        k_patch_setup_simple<<<(unsigned)std::min<int64_t>(np - p0, 1 << 30), 128>>>(ctx->g[l], c.nu, p0, p, d_st);
+        k_patch_setup_simple<<<(unsigned)std::min<int64_t>(np - p0, 1 << 30), 128>>>(ctx->g[l], c.nu, p0, p, d_st,
+                                                                                      np, 0);
       CKL();
     }
     int hst = 0;
@@ -1160,6 +1233,19 @@ int create_impl(svk_ctx* ctx) {
         double* p;
         TRY(alloc_vec(ctx, &p, np));
         v->push_back(p);
+      }
+    }
+  }
+  if (c.validate) {  // validation mode: every patch of every level against its group
+    for (int l = 0; l < ctx->nlev; ++l) {
+      double dev = 0.0;
+      int64_t n = 0;
+      TRY(op_validate(ctx, l, &dev, &n));
+      if (!(dev <= kValidateTol)) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "validation: patch inverses deviate from their group by %.3e on level %d", dev, l);
+        ctx->err = buf;
+        return SVK_ERR_VALIDATION;
       }
     }
   }
@@ -1527,6 +1613,25 @@ int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y,
   });
 }
 
+int svk_validate_patches(svk_ctx* ctx, int32_t level, double* max_rel_dev, int64_t* n_patches) {
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    double dev = 0.0;
+    int64_t n = 0;
+    TRY(op_validate(ctx, level, &dev, &n));
+    if (max_rel_dev) *max_rel_dev = dev;
+    if (n_patches) *n_patches = n;
+    if (!(dev <= kValidateTol)) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "validation: patch inverses deviate from their group by %.3e (> %.0e) on level %d",
+                    dev, kValidateTol, level);
+      ctx->err = buf;
+      return SVK_ERR_VALIDATION;
+    }
+    return SVK_OK;
+  });
+}
+
 int64_t svk_launch_count(const svk_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 int svk_set_profiling(svk_ctx* ctx, int32_t enable) {
@@ -1610,6 +1715,7 @@ const char* svk_status_string(int status) {
     case SVK_ERR_SINGULAR: return "singular factorisation";
     case SVK_ERR_NONFINITE: return "non-finite value";
     case SVK_ERR_ALLOC: return "allocation failed";
+    case SVK_ERR_VALIDATION: return "patch validation failed";
     default: return "unknown status";
   }
 }

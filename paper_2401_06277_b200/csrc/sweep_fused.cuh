@@ -1046,6 +1046,61 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
   mbar_wait(&bars[bl], (phases >> bl) & 1u);
 }
 
+// -----------------------------------------------------------------------------
+// Validation mode ("only 25 different patch matrices",
+// S:391).  Tuned Vanka stores one inverse per group (category pair) and, for
+// the generic group, the reflection-basis Schur factors; validation rebuilds
+// every patch's own inverse (k_patch_setup_simple, in batches) and compares it
+// with the stored inverse of its group, and applies the generic factors to the
+// 51 unit vectors and compares the result with the generic group's inverse.
+// Deviations are |a - b| / max|group inverse|, maximised with an atomicMax on
+// the bit pattern (monotone for non-negative doubles).
+// -----------------------------------------------------------------------------
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+// batch entry (q, i): patch p0 + i, slot pair q = r * 51 + c
+__global__ void k_validate_batch(LevelGeom g, int64_t p0, int64_t nb, const double* __restrict__ batch,
+                                 const double* __restrict__ ginv, const double* __restrict__ gscale,
+                                 double* __restrict__ maxdev) {
+  const int N = g.N;
+  const int64_t np = (int64_t)(N + 1) * (N + 1);
+  double dev = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nb * kGroupStride;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % nb, q = e / nb, p = p0 + i;
+    if (p >= np) continue;
+    const int kx = (int)(p % (N + 1)), ky = (int)(p / (N + 1));
+    const int grp = pcat(ky, N) * 5 + pcat(kx, N);
+    const double d = fabs(batch[q * nb + i] - ginv[(int64_t)grp * kGroupStride + q]) / gscale[grp];
+    dev = d > dev ? d : dev;  // NaN-safe below: a NaN difference is reported as +inf
+    if (d != d) dev = INFINITY;
+  }
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(maxdev, dev);
+}
+// column q of the generic patch's inverse through the structured solve
+// (solve_generic_sym) vs the generic group's stored dense inverse
+__global__ void k_validate_factors(const FusedFactors F, const double* __restrict__ ginv12, double gscale,
+                                   double* __restrict__ maxdev) {
+  const int q = threadIdx.x;
+  if (q >= kSlots) return;
+  double vx[25], vy[25];
+#pragma unroll
+  for (int k = 0; k < 25; ++k) {
+    vx[k] = (q == k) ? 1.0 : 0.0;
+    vy[k] = (q == 25 + k) ? 1.0 : 0.0;
+  }
+  const double dp = solve_generic_sym(vx, vy, q == 50 ? 1.0 : 0.0, F);
+  double dev = 0.0;
+  for (int r = 0; r < kSlots; ++r) {
+    const double v = r < 25 ? vx[r] : (r < 50 ? vy[r - 25] : dp);
+    const double d = fabs(v - ginv12[r * kSlots + q]) / gscale;
+    dev = (d > dev || d != d) ? (d != d ? INFINITY : d) : dev;
+  }
+  atomic_max_nonneg(maxdev, dev);
+}
+
 inline int launch_factor_setup(const int* d_Ns, int nlev, double nu, const double* /*d_inv*/, double* d_fac,
                                int* d_status) {
   k_factor_setup<<<nlev, 256>>>(d_Ns, nu, d_fac, d_status);

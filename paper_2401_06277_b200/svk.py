@@ -40,7 +40,7 @@ class Config(C.Structure):
                 ("transport", C.c_int32), ("agglom_rows", C.c_int32), ("emul_group", C.c_int32),
                 ("orth", C.c_int32), ("relax", C.c_int32), ("jacobi_sweeps", C.c_int32), ("nccl_id", C.c_uint8 * 128),
                 ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double),
-                ("precond", C.c_int32), ("bt_cycles", C.c_int32), ("bt_nu", C.c_int32), ("bt_reserved", C.c_int32),
+                ("precond", C.c_int32), ("bt_cycles", C.c_int32), ("bt_nu", C.c_int32), ("validate", C.c_int32),
                 ("bt_omega_u", C.c_double), ("bt_omega_p", C.c_double)]
 
 
@@ -84,6 +84,7 @@ EXPORTS = {
     "svk_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                                  C.POINTER(Report), C.c_void_p]),
     "svk_patch_inverse": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
+    "svk_validate_patches": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "svk_launch_count": (C.c_int64, [C.c_void_p]),
     "svk_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "svk_sweep_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
@@ -154,7 +155,7 @@ class Solver:
                  orth: str = "adaptive", relax: str = "vanka", relax_t: float | None = None,
                  relax_omega: float | None = None, jacobi_omega: float | None = None,
                  jacobi_sweeps: int | None = None, precond: str = "mg", bt_cycles: int = 3, bt_nu: int = 3,
-                 bt_omega_u: float = 1.0, bt_omega_p: float = 0.6):
+                 bt_omega_u: float = 1.0, bt_omega_p: float = 0.6, validate: bool = False):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
         "emulated" runs nranks logical ranks of one process on one device (one thread each).
@@ -175,6 +176,7 @@ class Solver:
         cfg.relax = RELAX[relax]
         cfg.precond, cfg.bt_cycles, cfg.bt_nu = PRECOND[precond], bt_cycles, bt_nu
         cfg.bt_omega_u, cfg.bt_omega_p = bt_omega_u, bt_omega_p
+        cfg.validate = 1 if validate else 0
         if relax != "vanka":
             d = RELAX_DEFAULTS[relax]
             cfg.relax_t = d[0] if relax_t is None else relax_t
@@ -192,7 +194,7 @@ class Solver:
         h = C.c_void_p()
         st = self.lib.svk_create(C.byref(cfg), C.byref(h))
         if st != SVK_OK:
-            raise SvkError("svk_create failed: %s" % self.lib.svk_status_string(st).decode())
+            raise SvkError("svk_create failed: %s (%d)" % (self.lib.svk_status_string(st).decode(), st))
         self._h = h
         nl = C.c_int32()
         self.lib.svk_num_levels(self._h, C.byref(nl))
@@ -384,6 +386,17 @@ class Solver:
         self._chk(self.lib.svk_patch_inverse(self._h, level, cat_x, cat_y, out.ctypes.data_as(C.c_void_p),
                                              C.byref(n)))
         return out[: n.value * n.value].reshape(n.value, n.value).copy()
+
+    def validate_patches(self, level: int | None = None):
+        """Validation mode on one level (svk_validate_patches): (max relative deviation,
+        patch count); raises SvkError if a patch differs from its group by more than 1e-12."""
+        level = self.fine if level is None else level
+        dev, n = C.c_double(), C.c_int64()
+        st = self.lib.svk_validate_patches(self._h, level, C.byref(dev), C.byref(n))
+        if st < 0:
+            msg = self.lib.svk_last_error(self._h)
+            raise SvkError("%s: %s" % (self.lib.svk_status_string(st).decode(), msg.decode() if msg else ""))
+        return dev.value, n.value
 
     def set_profiling(self, on: bool = True):
         self._chk(self.lib.svk_set_profiling(self._h, 1 if on else 0))
