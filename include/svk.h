@@ -321,6 +321,14 @@ int svk_patch_inverse(svk_ctx* ctx, int32_t level, int32_t cat_x, int32_t cat_y,
  * deviation); workspace ~170 MB, freed on return. */
 int svk_validate_patches(svk_ctx* ctx, int32_t level, double* max_rel_dev, int64_t* n_patches);
 
+/* Device memory held by the context (workspaces, Krylov basis, factors) in
+ * bytes, host out-parameter.  With nranks > 1 the vectors of the distributed
+ * levels are SLAB-LOCAL: their full pitched layout is reserved as virtual
+ * address space but device memory is mapped only for the rank's slab, its halo
+ * and a 2-node-row margin (SVK_SLAB_LOCAL=0 allocates them full size), so a
+ * rank holds ~1/nranks of each such vector. */
+int svk_device_bytes(const svk_ctx* ctx, int64_t* bytes);
+
 int64_t svk_launch_count(const svk_ctx* ctx);
 
 /* Benchmark support.  While profiling is enabled, every full Vanka sweep (non-

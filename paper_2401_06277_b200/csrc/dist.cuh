@@ -16,8 +16,11 @@
 //    thread per rank): the same operations through a shared group object,
 //    device-to-device copies and a host barrier.  Test mode only.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+
+#include <algorithm>
 
 #include <condition_variable>
 #include <cstdint>
@@ -38,6 +41,130 @@ inline void slab_rows(int N, int Nla, int nranks, int rank, int* r0, int* r1) {
   *r1 = rank == nranks - 1 ? N + 1 : (int)(((int64_t)(rank + 1) * Nla / nranks) * s);
 }
 
+// ----------------------------------------------------------------- slab-local memory
+// Virtual-memory-managed vectors: the whole pitched vector is reserved as
+// address space and device memory is created and mapped only for given byte
+// ranges (rounded to the allocation granularity).  Driver entry points are
+// fetched with cudaGetDriverEntryPoint (no link-time libcuda dependency).
+struct SlabMem {
+  uintptr_t base = 0;
+  size_t reserved = 0;
+  std::vector<std::pair<int64_t, int64_t>> maps;  // (offset, bytes) of each mapped range
+  std::vector<unsigned long long> handles;        // CUmemGenericAllocationHandle per range
+  int64_t mapped = 0;
+};
+struct VmmApi {
+  CUresult (*AddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*AddressFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*Create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*Release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*Map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*Unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*SetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*Granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  bool ok() const { return AddressReserve && AddressFree && Create && Release && Map && Unmap && SetAccess && Granularity; }
+};
+inline VmmApi& vmm_api() {
+  static VmmApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* n) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(n, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return p;
+    };
+    a.AddressReserve = (decltype(a.AddressReserve))get("cuMemAddressReserve");
+    a.AddressFree = (decltype(a.AddressFree))get("cuMemAddressFree");
+    a.Create = (decltype(a.Create))get("cuMemCreate");
+    a.Release = (decltype(a.Release))get("cuMemRelease");
+    a.Map = (decltype(a.Map))get("cuMemMap");
+    a.Unmap = (decltype(a.Unmap))get("cuMemUnmap");
+    a.SetAccess = (decltype(a.SetAccess))get("cuMemSetAccess");
+    a.Granularity = (decltype(a.Granularity))get("cuMemGetAllocationGranularity");
+  });
+  return a;
+}
+inline void slab_free(SlabMem& m) {
+  VmmApi& a = vmm_api();
+  for (size_t k = 0; k < m.maps.size(); ++k) {
+    if (k < m.handles.size()) {
+      a.Unmap((CUdeviceptr)(m.base + m.maps[k].first), (size_t)m.maps[k].second);
+      a.Release((CUmemGenericAllocationHandle)m.handles[k]);
+    }
+  }
+  if (m.base) a.AddressFree((CUdeviceptr)m.base, m.reserved);
+  m = SlabMem{};
+}
+// reserve `bytes` of address space on `device` and map the byte ranges `want`
+inline int slab_alloc(int device, int64_t bytes, std::vector<std::pair<int64_t, int64_t>> want, SlabMem* out,
+                      std::string& err) {
+  VmmApi& a = vmm_api();
+  if (!a.ok()) {
+    err = "CUDA virtual memory management entry points unavailable";
+    return -1;
+  }
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  size_t gran = 0;
+  if (a.Granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || gran == 0) {
+    err = "cuMemGetAllocationGranularity failed";
+    return -1;
+  }
+  const int64_t G = (int64_t)gran;
+  SlabMem m;
+  m.reserved = (size_t)((bytes + G - 1) / G * G);
+  CUdeviceptr base = 0;
+  if (a.AddressReserve(&base, m.reserved, (size_t)G, 0, 0) != CUDA_SUCCESS) {
+    err = "cuMemAddressReserve failed";
+    return -1;
+  }
+  m.base = (uintptr_t)base;
+  // round to the granularity, sort, merge
+  for (auto& r : want) {
+    const int64_t lo = r.first / G * G, hi = std::min<int64_t>((r.second + G - 1) / G * G, (int64_t)m.reserved);
+    r = {lo, hi};
+  }
+  std::sort(want.begin(), want.end());
+  std::vector<std::pair<int64_t, int64_t>> merged;
+  for (const auto& r : want) {
+    if (r.second <= r.first) continue;
+    if (!merged.empty() && r.first <= merged.back().second) merged.back().second = std::max(merged.back().second, r.second);
+    else merged.push_back(r);
+  }
+  CUmemAccessDesc acc{};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (const auto& r : merged) {
+    const size_t sz = (size_t)(r.second - r.first);
+    CUmemGenericAllocationHandle h;
+    if (a.Create(&h, sz, &prop, 0) != CUDA_SUCCESS) {
+      err = "cuMemCreate failed (device memory exhausted?)";
+      slab_free(m);
+      return -1;
+    }
+    if (a.Map((CUdeviceptr)(m.base + r.first), sz, 0, h, 0) != CUDA_SUCCESS) {
+      a.Release(h);
+      err = "cuMemMap failed";
+      slab_free(m);
+      return -1;
+    }
+    m.maps.push_back({r.first, (int64_t)sz});
+    m.handles.push_back((unsigned long long)h);
+    m.mapped += (int64_t)sz;
+    if (a.SetAccess((CUdeviceptr)(m.base + r.first), sz, &acc, 1) != CUDA_SUCCESS) {
+      err = "cuMemSetAccess failed";
+      slab_free(m);
+      return -1;
+    }
+  }
+  *out = m;
+  return 0;
+}
+
 // A contiguous block of doubles to send / receive.
 struct Block {
   double* ptr;
@@ -53,6 +180,11 @@ class Transport {
                        const std::vector<Block>& hi_send, const std::vector<Block>& hi_recv, cudaStream_t s,
                        std::string& err) = 0;
   virtual int allreduce_sum(double* buf, int64_t count, cudaStream_t s, std::string& err) = 0;
+  // recv[r * count .. (r+1) * count) = rank r's send[0 .. count) for every rank r
+  // (send may alias recv + rank * count)
+  virtual int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) = 0;
+  // whether its operations may be captured into a CUDA graph (stream-ordered, no host sync)
+  virtual bool capturable() const = 0;
 };
 
 // ----------------------------------------------------------------- NCCL
@@ -69,10 +201,13 @@ struct NcclApi {
   ncclResult_t_ (*Send)(const void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
   ncclResult_t_ (*Recv)(void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
   ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*AllGather)(const void*, void*, size_t, int, ncclComm_t_, cudaStream_t) = nullptr;
   ncclResult_t_ (*GroupStart)() = nullptr;
   ncclResult_t_ (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t_) = nullptr;
-  bool ok() const { return h && GetUniqueId && CommInitRank && Send && Recv && AllReduce && GroupStart && GroupEnd; }
+  bool ok() const {
+    return h && GetUniqueId && CommInitRank && Send && Recv && AllReduce && AllGather && GroupStart && GroupEnd;
+  }
 };
 inline NcclApi& nccl_api() {
   static NcclApi api;
@@ -90,6 +225,7 @@ inline NcclApi& nccl_api() {
     api.Send = (decltype(api.Send))dlsym(api.h, "ncclSend");
     api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
     api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+    api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
     api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
@@ -145,6 +281,14 @@ class NcclTransport : public Transport {
     }
     return 0;
   }
+  bool capturable() const override { return true; }  // NCCL operations are stream-capturable
+  int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) override {
+    if (nccl_api().AllGather(send, recv, (size_t)count, kNcclDouble, comm_, s) != 0) {
+      err = "ncclAllGather failed";
+      return -1;
+    }
+    return 0;
+  }
 
  private:
   int rank_, nranks_;
@@ -162,7 +306,8 @@ struct EmulGroup {
   // per-rank slots for the current collective
   std::vector<std::vector<Block>> lo_send, hi_send;
   std::vector<std::vector<double>> red;
-  explicit EmulGroup(int n) : nranks(n), lo_send(n), hi_send(n), red(n) {}
+  std::vector<const double*> gsend;
+  explicit EmulGroup(int n) : nranks(n), lo_send(n), hi_send(n), red(n), gsend(n, nullptr) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const int64_t gen = generation;
@@ -230,6 +375,22 @@ class EmulTransport : public Transport {
     G.barrier();
     cudaMemcpy(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice);
     return 0;
+  }
+  bool capturable() const override { return false; }  // host barriers
+  int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      err = "emulated allgather: stream sync failed";
+      return -1;
+    }
+    EmulGroup& G = *group_;
+    std::vector<double> mine((size_t)count);  // a copy, so that send may alias recv
+    cudaMemcpy(mine.data(), send, count * sizeof(double), cudaMemcpyDeviceToHost);
+    G.red[rank_] = mine;
+    G.barrier();
+    for (int r = 0; r < G.nranks; ++r)
+      cudaMemcpy(recv + (int64_t)r * count, G.red[r].data(), count * sizeof(double), cudaMemcpyHostToDevice);
+    G.barrier();
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
 
  private:

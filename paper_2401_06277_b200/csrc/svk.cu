@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -90,6 +91,14 @@ struct svk_ctx {
   int use_graphs = -1;                  // -1: decide at first use (SVK_GRAPHS=0 disables)
   double prof_acc_ms = 0.0;
   int64_t prof_acc_n = 0;
+  // device memory the context holds (cudaMalloc'd bytes + physically mapped
+  // bytes of slab-local vectors), svk_device_bytes
+  double* d_agg = nullptr;  // agglomeration staging: nranks chunks of the coarse slab pieces
+  int64_t agg_cap = 0;
+  bool slab_local = true;  // distributed-level workspaces slab-local (SVK_SLAB_LOCAL=0: full size)
+  int64_t dev_bytes = 0;
+  std::map<const double*, int64_t> plain_bytes;  // cudaMalloc'd vectors -> bytes
+  std::map<const double*, SlabMem> slab_mem;     // slab-local vectors (distributed levels)
   // multi-GPU row slabs (dist.cuh): levels la..nlev-1 are distributed
   std::unique_ptr<Transport> tr;
   int la = 1 << 30;
@@ -267,7 +276,26 @@ int valid_ptr(svk_ctx* ctx, const void* p, const char* what) {
 int alloc_vec(svk_ctx* ctx, double** p, int64_t n) {
   CK(cudaMalloc(p, n * sizeof(double)));
   CK(cudaMemset(*p, 0, n * sizeof(double)));
+  ctx->dev_bytes += n * (int64_t)sizeof(double);
+  ctx->plain_bytes[*p] = n * (int64_t)sizeof(double);
   return SVK_OK;
+}
+// release a vector from alloc_vec / alloc_level_vec
+void free_vec(svk_ctx* ctx, double* p) {
+  if (!p) return;
+  auto it = ctx->slab_mem.find(p);
+  if (it != ctx->slab_mem.end()) {
+    ctx->dev_bytes -= it->second.mapped;
+    slab_free(it->second);
+    ctx->slab_mem.erase(it);
+    return;
+  }
+  auto jt = ctx->plain_bytes.find(p);
+  if (jt != ctx->plain_bytes.end()) {
+    ctx->dev_bytes -= jt->second;
+    ctx->plain_bytes.erase(jt);
+  }
+  cudaFree(p);
 }
 
 // ------------------------------------------------------------------ level ops
@@ -305,6 +333,63 @@ Block plane_rows(double* v, int64_t off, int64_t pitch, int a, int b) {
   return Block{v + off + (int64_t)a * pitch, (int64_t)std::max(0, b - a) * pitch};
 }
 
+// Rows of each plane a rank's kernels may touch on a distributed level: its
+// slab plus the halo (kHalo node rows) and a margin of 2 node rows; lattice rows
+// [ua, ub) of the velocity planes, node rows [pa, pb) of the pressure plane.
+struct SlabRows {
+  int ua, ub, pa, pb;
+};
+SlabRows slab_rows_touched(const LevelGeom& g) {
+  const int m = kHalo + 2;
+  return SlabRows{std::max(0, 2 * (g.r0 - m)), std::min(g.lat, 2 * (g.r1 + m)), std::max(0, g.r0 - m),
+                  std::min(g.N + 1, g.r1 + m)};
+}
+// Slab-local vector of a distributed level: the full pitched
+// layout is reserved as virtual address space, but device memory is mapped only
+// for the rows the rank touches, so every kernel keeps global row indexing while
+// a rank holds ~1/P of the vector (plus halos).  Replicated levels: alloc_vec.
+int alloc_level_vec(svk_ctx* ctx, int l, double** p) {
+  const LevelGeom& g = ctx->g[l];
+  if (!dist_level(ctx, l) || !ctx->slab_local) return alloc_vec(ctx, p, g.len);
+  const SlabRows R = slab_rows_touched(g);
+  const int64_t b8 = (int64_t)sizeof(double);
+  std::vector<std::pair<int64_t, int64_t>> ranges = {
+      {(g.oux + (int64_t)R.ua * g.pu) * b8, (g.oux + (int64_t)R.ub * g.pu) * b8},
+      {(g.ouy + (int64_t)R.ua * g.pu) * b8, (g.ouy + (int64_t)R.ub * g.pu) * b8},
+      {(g.op + (int64_t)R.pa * g.pp) * b8, (g.op + (int64_t)R.pb * g.pp) * b8}};
+  SlabMem m;
+  std::string err;
+  if (slab_alloc(ctx->cfg.device, g.len * b8, ranges, &m, err) != 0) {
+    ctx->err = "slab-local vector: " + err;
+    return SVK_ERR_ALLOC;
+  }
+  *p = reinterpret_cast<double*>(m.base);
+  for (const auto& r : m.maps) CK(cudaMemset(reinterpret_cast<char*>(m.base) + r.first, 0, r.second));
+  ctx->dev_bytes += m.mapped;
+  ctx->slab_mem[*p] = m;
+  return SVK_OK;
+}
+// the byte ranges of v that hold device memory (the whole vector unless slab-local)
+std::vector<std::pair<int64_t, int64_t>> vec_ranges(const svk_ctx* ctx, const double* v, int64_t len) {
+  auto it = ctx->slab_mem.find(v);
+  if (it == ctx->slab_mem.end()) return {{0, len * (int64_t)sizeof(double)}};
+  return it->second.maps;
+}
+// x = 0 / y = x over the memory both vectors hold on level l
+int op_zero_level(svk_ctx* ctx, int l, double* x, cudaStream_t s) {
+  for (const auto& r : vec_ranges(ctx, x, ctx->g[l].len))
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(x) + r.first, 0, r.second, s));
+  return SVK_OK;
+}
+int op_copy_level(svk_ctx* ctx, int l, double* y, const double* x, cudaStream_t s) {
+  const bool sy = ctx->slab_mem.count(y), sx = ctx->slab_mem.count(x);
+  const auto ranges = vec_ranges(ctx, sy ? y : x, ctx->g[l].len);  // slab maps of one level are identical
+  for (const auto& r : (sy || sx) ? ranges : vec_ranges(ctx, y, ctx->g[l].len))
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(y) + r.first, reinterpret_cast<const char*>(x) + r.first, r.second,
+                       cudaMemcpyDeviceToDevice, s));
+  return SVK_OK;
+}
+
 // refresh the halo rows of v on level l from the neighbouring ranks
 int op_halo(svk_ctx* ctx, int l, double* v, cudaStream_t s) {
   if (!dist_level(ctx, l)) return SVK_OK;
@@ -327,15 +412,18 @@ int op_halo(svk_ctx* ctx, int l, double* v, cudaStream_t s) {
   }
   if (ctx->tr->exchange(ls, lr, hs, hr, s, ctx->err) != 0) return SVK_ERR_NCCL;
   ctx->launches++;
-  if (ctx->poison) {  // rows no kernel may read: NaN (0xFF bytes)
+  if (ctx->poison) {  // rows no kernel may read: NaN (0xFF bytes); a slab-local vector
+                      // holds no memory beyond its margin rows, so only those are poisoned
     const int ua = std::max(0, 2 * lo - 2 * H), ub = std::min(lat, 2 * hi + 2 * H);
     const int pa = std::max(0, lo - H), pb = std::min(np, hi + H);
+    const bool slab = ctx->slab_mem.count(v) != 0;
+    const SlabRows T = slab ? slab_rows_touched(g) : SlabRows{0, lat, 0, np};
     for (int64_t off : {g.oux, g.ouy}) {
-      CK(cudaMemsetAsync(v + off, 0xFF, (size_t)ua * g.pu * sizeof(double), s));
-      CK(cudaMemsetAsync(v + off + (int64_t)ub * g.pu, 0xFF, (size_t)(lat - ub) * g.pu * sizeof(double), s));
+      CK(cudaMemsetAsync(v + off + (int64_t)T.ua * g.pu, 0xFF, (size_t)std::max(0, ua - T.ua) * g.pu * sizeof(double), s));
+      CK(cudaMemsetAsync(v + off + (int64_t)ub * g.pu, 0xFF, (size_t)std::max(0, T.ub - ub) * g.pu * sizeof(double), s));
     }
-    CK(cudaMemsetAsync(v + g.op, 0xFF, (size_t)pa * g.pp * sizeof(double), s));
-    CK(cudaMemsetAsync(v + g.op + (int64_t)pb * g.pp, 0xFF, (size_t)(np - pb) * g.pp * sizeof(double), s));
+    CK(cudaMemsetAsync(v + g.op + (int64_t)T.pa * g.pp, 0xFF, (size_t)std::max(0, pa - T.pa) * g.pp * sizeof(double), s));
+    CK(cudaMemsetAsync(v + g.op + (int64_t)pb * g.pp, 0xFF, (size_t)std::max(0, T.pb - pb) * g.pp * sizeof(double), s));
   }
   return SVK_OK;
 }
@@ -606,6 +694,63 @@ int op_coarse(svk_ctx* ctx, const double* b, double* x, cudaStream_t s) {
   return SVK_OK;
 }
 
+// Agglomeration: level l is the coarsest distributed level and
+// level l-1 is replicated.  Each rank has restricted its slab's coarse rows into
+// rc (the halves of its fine slab, op_residual_restrict); the three plane pieces
+// are packed into one fixed-size chunk, all-gathered (each rank receives the
+// other ranks' rows once: (P-1)/P of the coarse vector, half the bytes of an
+// all-reduce of zero-padded copies) and unpacked into every rank's full rc.
+int op_agglomerate(svk_ctx* ctx, int l, double* rc, cudaStream_t s) {
+  const LevelGeom& gf = ctx->g[l];
+  const LevelGeom& gc = ctx->g[l - 1];
+  const int P = ctx->cfg.nranks;
+  const int Nla = ctx->g[ctx->la].N;
+  // coarse node rows of rank r: the halves of its fine slab (as op_residual_restrict)
+  std::vector<int> c0(P), c1(P);
+  int64_t K = 0;
+  for (int r = 0; r < P; ++r) {
+    int f0, f1;
+    slab_rows(gf.N, Nla, P, r, &f0, &f1);
+    c0[r] = f0 / 2;
+    c1[r] = f1 == gf.N + 1 ? gc.N + 1 : f1 / 2;
+    const int64_t u = (int64_t)(std::min(2 * c1[r], gc.lat) - std::min(2 * c0[r], gc.lat)) * gc.pu;
+    K = std::max<int64_t>(K, 2 * u + (int64_t)(c1[r] - c0[r]) * gc.pp);
+  }
+  if (ctx->agg_cap < (int64_t)P * K) {
+    if (ctx->d_agg) cudaFree(ctx->d_agg);
+    ctx->d_agg = nullptr;
+    CK(cudaMalloc(&ctx->d_agg, (size_t)P * K * sizeof(double)));
+    ctx->agg_cap = (int64_t)P * K;
+  }
+  auto pieces = [&](int r, double* v, std::vector<Block>& out) {
+    const int ua = std::min(2 * c0[r], gc.lat), ub = std::min(2 * c1[r], gc.lat);
+    out = {plane_rows(v, gc.oux, gc.pu, ua, ub), plane_rows(v, gc.ouy, gc.pu, ua, ub),
+           plane_rows(v, gc.op, gc.pp, c0[r], c1[r])};
+  };
+  const int me = ctx->cfg.rank;
+  std::vector<Block> bl;
+  pieces(me, rc, bl);
+  double* mine = ctx->d_agg + (int64_t)me * K;
+  int64_t o = 0;
+  for (const Block& b : bl) {
+    if (b.count) CK(cudaMemcpyAsync(mine + o, b.ptr, b.count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    o += b.count;
+  }
+  if (ctx->tr->allgather(mine, ctx->d_agg, K, s, ctx->err) != 0) return SVK_ERR_NCCL;
+  ctx->launches++;
+  for (int r = 0; r < P; ++r) {
+    if (r == me) continue;
+    pieces(r, rc, bl);
+    const double* src = ctx->d_agg + (int64_t)r * K;
+    int64_t q = 0;
+    for (const Block& b : bl) {
+      if (b.count) CK(cudaMemcpyAsync(b.ptr, src + q, b.count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      q += b.count;
+    }
+  }
+  return SVK_OK;
+}
+
 // alg:mg on level l; x in/out; x_zero: x is known to be 0 on entry
 // Distributed levels (row slabs): every operation computes the owned rows; the
 // halos of b (on entry), of x after every relaxation and after the correction,
@@ -628,11 +773,10 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
     std::swap(cur, oth);
     if (D) TRY(op_halo(ctx, l, cur, s));
   }
-  if (ctx->cfg.nu_pre == 0 && x_zero) CK(cudaMemsetAsync(cur, 0, g.len * sizeof(double), s));
+  if (ctx->cfg.nu_pre == 0 && x_zero) TRY(op_zero_level(ctx, l, cur, s));
   const bool agglomerate = D && !dist_level(ctx, l - 1);
-  if (agglomerate) CK(cudaMemsetAsync(ctx->ws_b[l - 1], 0, ctx->g[l - 1].len * sizeof(double), s));
   TRY(op_residual_restrict(ctx, l, cur, b, ctx->ws_b[l - 1], s));  // "Compute residual" + "Restriction"
-  if (agglomerate) TRY(op_allreduce(ctx, ctx->ws_b[l - 1], ctx->g[l - 1].len, s));
+  if (agglomerate) TRY(op_agglomerate(ctx, l, ctx->ws_b[l - 1], s));
   TRY(op_mg(ctx, l - 1, ctx->ws_b[l - 1], ctx->ws_x[l - 1], true, s));  // A_0^{-1} or MG(l-1)
   TRY(op_prolong_add(ctx, l, ctx->ws_x[l - 1], cur, s));       // "Correction"
   if (D) TRY(op_halo(ctx, l, cur, s));
@@ -641,7 +785,7 @@ int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStre
     std::swap(cur, oth);
     if (D) TRY(op_halo(ctx, l, cur, s));
   }
-  if (cur != x) CK(cudaMemcpyAsync(x, cur, g.len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (cur != x) TRY(op_copy_level(ctx, l, x, cur, s));
   return SVK_OK;
 }
 
@@ -718,16 +862,17 @@ int harvest_graph_prof(svk_ctx* ctx) {
 
 // z = M v (one V-cycle from zero on the finest level) for FGMRES: replayed from a
 // CUDA graph captured on the library's own stream at the first use of the pair
-// (v, z); single-GPU contexts only (the emulated transport synchronises host
+// (v, z); not with the emulated transport (it synchronises host
 // threads inside a cycle, which a graph cannot hold).  Falls back to direct
-// launches if capture is unavailable.
+// launches if capture is unavailable.  Multi-GPU (NCCL): the cycle's halo
+// exchanges and the agglomeration all-gather are captured with it.
 int op_precond_mg(svk_ctx* ctx, const double* v, double* z, cudaStream_t s) {
   const int L = ctx->nlev - 1;
   if (ctx->use_graphs < 0) {
     const char* e = std::getenv("SVK_GRAPHS");
     ctx->use_graphs = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!ctx->use_graphs || ctx->tr) return op_mg(ctx, L, v, z, true, s);
+  if (!ctx->use_graphs || (ctx->tr && !ctx->tr->capturable())) return op_mg(ctx, L, v, z, true, s);
   svk_ctx::GraphRec* gr = nullptr;
   for (auto& g : ctx->graphs)
     if (g->in == v && g->out == z && g->prof == ctx->prof) gr = g.get();
@@ -849,12 +994,12 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   // coefficient area: [c1 (maxit+1) | c2 (maxit+1) | raw (maxit+1) | nrm | n^-2 (maxit+1)]
   const int o1 = 0, o2 = maxit + 1, oraw = 2 * (maxit + 1), onrm = 3 * (maxit + 1), oinv = 3 * (maxit + 1) + 1;
   TRY(ensure_coef(ctx, 4 * (maxit + 1) + 8));
-  if (!ctx->d_w) TRY(alloc_vec(ctx, &ctx->d_w, n));
-  if (!ctx->d_r) TRY(alloc_vec(ctx, &ctx->d_r, n));
+  if (!ctx->d_w) TRY(alloc_level_vec(ctx, L, &ctx->d_w));
+  if (!ctx->d_r) TRY(alloc_level_vec(ctx, L, &ctx->d_r));
   auto ensure_vec = [&](std::vector<double*>& pool, int k) -> int {
     while ((int)pool.size() <= k) {
       double* p;
-      TRY(alloc_vec(ctx, &p, n));
+      TRY(alloc_level_vec(ctx, L, &p));
       pool.push_back(p);
     }
     return SVK_OK;
@@ -1010,12 +1155,12 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_cmat);
   F(ctx->d_cidx);
   for (auto* v : {&ctx->ws_x, &ctx->ws_t, &ctx->ws_r, &ctx->ws_b})
-    for (double* p : *v) F(p);
+    for (double* p : *v) free_vec(ctx, p);
   F(ctx->d_dbuf);
   for (double* p : ctx->d_inv_simple) F(p);
   F(ctx->d_bd);
   for (BdTile* p : ctx->d_tiles) F(p);
-  F(ctx->d_sw);
+  free_vec(ctx, ctx->d_sw);
   F(ctx->d_schur);
   F(ctx->d_btb);
   F(ctx->d_bt_invL);
@@ -1024,10 +1169,11 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_bt_idxM);
   for (auto* v : {&ctx->p_rhs, &ctx->p_dp0, &ctx->p_dp1})
     for (double* p : *v) F(p);
-  for (double* p : ctx->V) F(p);
-  for (double* p : ctx->Z) F(p);
-  F(ctx->d_w);
-  F(ctx->d_r);
+  for (double* p : ctx->V) free_vec(ctx, p);
+  for (double* p : ctx->Z) free_vec(ctx, p);
+  F(ctx->d_agg);
+  free_vec(ctx, ctx->d_w);
+  free_vec(ctx, ctx->d_r);
   F(ctx->d_part);
   F(ctx->d_coef);
   F(ctx->d_hb);
@@ -1086,6 +1232,8 @@ int create_impl(svk_ctx* ctx) {
     }
     const char* pz = std::getenv("SVK_POISON_HALO");
     ctx->poison = pz && pz[0] == '1';
+    const char* sl = std::getenv("SVK_SLAB_LOCAL");
+    ctx->slab_local = !(sl && sl[0] == '0');
   }
   CK(cudaMalloc(&ctx->d_Ns, Ns.size() * sizeof(int)));
   CK(cudaMemcpy(ctx->d_Ns, Ns.data(), Ns.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -1150,13 +1298,12 @@ int create_impl(svk_ctx* ctx) {
   ctx->ws_r.assign(ctx->nlev, nullptr);
   ctx->ws_b.assign(ctx->nlev, nullptr);
   for (int l = 0; l < ctx->nlev; ++l) {
-    const int64_t n = ctx->g[l].len;
     if (l < ctx->nlev - 1) {
-      TRY(alloc_vec(ctx, &ctx->ws_x[l], n));
-      TRY(alloc_vec(ctx, &ctx->ws_b[l], n));
+      TRY(alloc_level_vec(ctx, l, &ctx->ws_x[l]));
+      TRY(alloc_level_vec(ctx, l, &ctx->ws_b[l]));
     }
-    TRY(alloc_vec(ctx, &ctx->ws_t[l], n));
-    TRY(alloc_vec(ctx, &ctx->ws_r[l], n));
+    TRY(alloc_level_vec(ctx, l, &ctx->ws_t[l]));
+    TRY(alloc_level_vec(ctx, l, &ctx->ws_r[l]));
   }
   TRY(alloc_vec(ctx, &ctx->d_bd, (int64_t)kSlots * bd_count(ctx->g.back().N)));
   for (int l = 0; l < ctx->nlev; ++l) {
@@ -1449,7 +1596,7 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
     TRY(op_halo(ctx, level, const_cast<double*>(b), s));
     TRY(op_halo(ctx, level, const_cast<double*>(x_in), s));
     if (nsweeps == 1) return op_sweep(ctx, level, x_in, b, x_out, false, s);
-    if (!ctx->d_sw) TRY(alloc_vec(ctx, &ctx->d_sw, ctx->g.back().len));
+    if (!ctx->d_sw) TRY(alloc_level_vec(ctx, ctx->nlev - 1, &ctx->d_sw));
     // ping-pong so that the last sweep lands in x_out
     double* bufs[2] = {x_out, ctx->d_sw};
     int dst = (nsweeps % 2 == 1) ? 0 : 1;
@@ -1630,6 +1777,12 @@ int svk_validate_patches(svk_ctx* ctx, int32_t level, double* max_rel_dev, int64
     }
     return SVK_OK;
   });
+}
+
+int svk_device_bytes(const svk_ctx* ctx, int64_t* bytes) {
+  if (!ctx || !bytes) return SVK_ERR_INVALID;
+  *bytes = ctx->dev_bytes;
+  return SVK_OK;
 }
 
 int64_t svk_launch_count(const svk_ctx* ctx) { return ctx ? ctx->launches : -1; }

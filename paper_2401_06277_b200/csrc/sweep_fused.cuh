@@ -781,13 +781,20 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
   // W_i = omega / (patches holding the point): 3 per axis at even, 2 at odd lattice indices
   const int i0 = 2 * kxp;
   const bool cin0 = i0 >= 1 && i0 <= lat - 2, cin1 = i0 + 1 <= lat - 2;
-  const bool cval0 = i0 <= lat - 1, cval1 = i0 + 1 <= lat - 1;
+  // Output weights with the column mask folded in (hoisted out of the step
+  // loop): 0 on Dirichlet and padding columns, where x_out = x_in + 0 keeps the
+  // boundary value (padding columns arrive as TMA zero fill and stay 0).
   double wgt[2][2];  // [row parity][column parity]
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
-      wgt[a][b] = A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0);
+      wgt[a][b] = (b ? cin1 : cin0)
+                      ? (A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0))
+                      : 0.0;
+  const bool colout = owner && 2 * kxp < g.pu;
+  double* const out_u = A.xout + g.oux + i0;  // dereferenced only when colout
+  double* const out_v = A.xout + g.ouy + i0;
   RingFzS S = RingFzS::at(sB);
   double pmw[3][3];  // pressure window rolled across steps
   for (int s = sB; s <= sE; ++s) {
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
     // ---- sum_i V_i^T delta_i on this lane's columns, lattice rows 2s-2 .. 2s+2,
     //      and x_out on rows 2s-2, 2s-1 (node row s-1), which are now complete ----
     const int ny = s - 1;
-    const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
+    const bool rowout = colout && ny >= y0 && ny < y1;  // the row test is uniform over the CTA
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const double* v = c ? vy : vx;
@@ -877,21 +884,15 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
         carry[r][c][1] = S1[r + 2];
       }
       if (rowout) {
+        double* const oc = (c ? out_v : out_u) + (int64_t)(2 * ny) * g.pu;
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int j = 2 * ny + rr;  // rr = row parity
-          if (j > lat - 1) continue;
-          const bool jin = j >= 1 && j <= lat - 2;
+          if (j > lat - 1) continue;  // uniform: the row past the last lattice row
+          const bool jin = j >= 1 && j <= lat - 2;  // uniform: Dirichlet rows keep x_in
           const double2 x = lds2(sm + S.xr(rr - 2, c) + 2 * pi + 4);
-          double o0, o1;
-          if (jin && cin0 && cin1) {  // interior (all but the outermost rows / columns)
-            o0 = fma(wgt[rr][0], S0[rr], x.x);
-            o1 = fma(wgt[rr][1], S1[rr], x.y);
-          } else {
-            o0 = (jin && cin0) ? fma(wgt[rr][0], S0[rr], x.x) : (cval0 ? x.x : 0.0);
-            o1 = (jin && cin1) ? fma(wgt[rr][1], S1[rr], x.y) : (cval1 ? x.y : 0.0);
-          }
-          *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) = make_double2(o0, o1);
+          const double w0 = jin ? wgt[rr][0] : 0.0, w1 = jin ? wgt[rr][1] : 0.0;
+          *reinterpret_cast<double2*>(oc + rr * g.pu) = make_double2(fma(w0, S0[rr], x.x), fma(w1, S1[rr], x.y));
         }
       }
     }

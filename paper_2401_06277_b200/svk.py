@@ -85,6 +85,7 @@ EXPORTS = {
                                  C.POINTER(Report), C.c_void_p]),
     "svk_patch_inverse": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
     "svk_validate_patches": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "svk_device_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "svk_launch_count": (C.c_int64, [C.c_void_p]),
     "svk_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "svk_sweep_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
@@ -406,6 +407,13 @@ class Solver:
         n, t = C.c_int64(), C.c_double()
         self._chk(self.lib.svk_sweep_stats(self._h, C.byref(n), C.byref(t)))
         return int(n.value), float(t.value)
+
+    @property
+    def device_bytes(self) -> int:
+        """Device memory held by the context (svk_device_bytes)."""
+        n = C.c_int64()
+        self._chk(self.lib.svk_device_bytes(self._h, C.byref(n)))
+        return int(n.value)
 
     @property
     def launch_count(self) -> int:

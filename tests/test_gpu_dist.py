@@ -155,7 +155,7 @@ def test_dist_vcycle(gpu, poison, P, N, agg, coarse):
         S.close()
 
 
-@pytest.mark.parametrize("P,N,agg", CASES + [(2, 64, 64)])
+@pytest.mark.parametrize("P,N,agg", CASES + [(2, 64, 64), (8, 512, 32)])
 def test_dist_fgmres_vs_oracle_and_single(gpu, poison, P, N, agg):
     from paper_2401_06277_b200 import Solver
     O = oracle.Oracle(N)
@@ -225,3 +225,33 @@ def test_dist_config_errors(gpu):
         Solver(64, rank=0, nranks=2, transport="emulated", agglom_rows=2)
     with pytest.raises(SvkError):
         Solver(64, rank=0, nranks=2, transport="emulated", sweep="unfused")
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_local_memory_per_rank(gpu, P):
+    """Distributed-level workspaces and the Krylov basis are slab-local: each rank
+    maps ~1/P of every such vector (plus halo, margin and page rounding), so a
+    rank's device memory is ~1/P of the single-GPU footprint (the replicated
+    coarse levels are small).  SVK_SLAB_LOCAL=0 would map them full size."""
+    from paper_2401_06277_b200 import Solver
+    N, its = 2048, 4
+    S1 = Solver(N)
+    b, x = S1.set_problem("mms_paper")
+    S1.fgmres(b, x, rtol=0.0, maxit=its)   # allocates its + 1 basis pairs
+    full = S1.device_bytes
+    S1.close()
+    del S1, b, x
+    Ss = make_solvers(P, N, 64)
+
+    def fn(r):
+        S = Ss[r]
+        b, x = S.set_problem("mms_paper")
+        S.fgmres(b, x, rtol=0.0, maxit=its)
+        return S.device_bytes
+
+    per_rank = run_ranks(P, fn)
+    for nb in per_rank:
+        assert nb < full * (1.0 / P + 0.12), (nb, full, P)
+    assert sum(per_rank) < full * 1.25
+    for S in Ss:
+        S.close()
