@@ -19,7 +19,8 @@ e2e    = the same solve through svk_solve_host with pinned HOST buffers (H2D of
          b and x0, D2H of x inside the timed region).
 --impl reference  times the CPU oracle (oracle/, C++ + OpenMP, fp64) on a bounded
          sample of the same workload (a 512^2 solve per step, the cpu_baseline's size) on the host cores.
-Multi-GPU (N > 1, torchrun): `--mode slabs` (default) splits the ONE 4096^2
+Multi-GPU (N > 1): one process per GPU under torchrun (bench.py relaunches itself
+under torch.distributed.run when WORLD_SIZE is unset): `--mode slabs` (default) splits the ONE 4096^2
 problem into N row slabs (libsvk multi-GPU mode over NCCL: halo exchanges,
 coarse-level agglomeration, all-reduced Krylov dots; strong scaling);
 `--mode replicas` solves an independent 4096^2 problem per rank (weak scaling).
@@ -316,6 +317,26 @@ def run_svk(args):
                                              "source": "profiles/r1_fp64_peak.json (tools/fp64_peak.cu)"}
     roofline["paper_equivalent_tflops"] = 5202 * nodes / t_sweep / 1e12
 
+    # second roofline entry: the FGMRES orthogonalisation (mat-vec + Gram-Schmidt
+    # multi-dot / multi-update kernels), HBM-bound.  Algorithmic vectors streamed
+    # per iteration j (m = j+1 basis vectors): mat-vec 2 (read z, write w),
+    # dots m+1 (V_0..V_j, w), update m+2 (V_0..V_j, w read; w' written); a
+    # second Gram-Schmidt pass adds m + (m+2).  Vector = owned rows incl. padding.
+    rep_last = reps[-1]
+    k_its, n_re = rep_last["iterations"], rep_last.get("n_reorth", 0)
+    lat = 2 * N + 1
+    vec_bytes = 8.0 * (2 * lat * ((lat + 7) // 8 * 8) + (N + 1) * ((N + 2 + 6) // 8 * 8)) * share
+    nvec = sum(2 + (j + 2) + (j + 3) for j in range(k_its))
+    # adaptive second passes: their iterations are not reported; charge them at the average m
+    nvec += n_re * (2 * ((k_its + 1) / 2) + 2)
+    orth_bytes = nvec * vec_bytes
+    t_orth = rep_last["t_orth_s"]
+    roofline_orth = {"bound": "hbm", "kernels": "k_residual_strip (mat-vec), k_cgs_dots, k_cgs_update, k_reduce_partials",
+                     "achieved": orth_bytes / t_orth / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": orth_bytes / t_orth / 1e9 / hbm_peak, "algorithmic_bytes": orth_bytes,
+                     "vectors_streamed": nvec, "t_s": t_orth, "peak_source": hbm_src,
+                     "traffic": "profiles/r2_krylov_ncu.json (DRAM bytes = algorithmic per launch)"}
+
     # end to end through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -357,10 +378,10 @@ def run_svk(args):
             "t_vcycle_s": reps[-1]["t_vcycle_s"], "t_orth_s": reps[-1]["t_orth_s"],
             "sweep": {"dof_per_s": n_dof(N) * share / t_sweep, "slab_share": share, "ms": 1e3 * t_sweep, "hbm_gbs_alg": sweep_gbs,
                       "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "roofline": roofline, "roofline_orth": roofline_orth, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         }
         if args.relax != "vanka" or args.precond != "mg":  # comparator line: no Vanka sweep in it
-            line["sweep"] = line["roofline"] = None
+            line["sweep"] = line["roofline"] = line["roofline_orth"] = None
         elif args.sweep != "fused":  # comparator line: the roofline accounting is the fused kernel's
             line["roofline"] = None
         print(json.dumps(line), flush=True)
@@ -400,6 +421,15 @@ def main():
         ap.error("--relax bs/su: single-GPU comparator runs of the svk arm only")
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this script under torchrun (the driver's own launch sets WORLD_SIZE)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_svk(args)

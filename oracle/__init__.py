@@ -79,6 +79,8 @@ def _load():
             "orc_fgmres": (I, [P, P, P, D, I, P, P, P]),
             "orc_sweep_sample": (None, [I, D, D, I, P, P, P, I64, P]),
             "orc_residual_sample": (None, [I, D, P, P, P, I64, P]),
+            "orc_restrict_residual_sample": (None, [I, D, P, P, P, I64, P]),
+            "orc_prolong_sample": (None, [I, P, P, P, I64, P]),
             "orc_set_relax": (I, [P, I, D, D, D, I]),
             "orc_relax_sweep": (None, [P, I, P, P, P]),
             "orc_schur_nnz": (I64, [P, I]),
@@ -127,6 +129,27 @@ def residual_sample(N: int, x, b, idx, nu: float = 1.0):
     idx = np.ascontiguousarray(idx, dtype=np.int64)
     out = np.zeros(len(idx))
     lib.orc_residual_sample(N, nu, _ptr(x), _ptr(b), _ptr(idx), len(idx), _ptr(out))
+    return out
+
+
+def restrict_residual_sample(Nf: int, x, b, idx, nu: float = 1.0):
+    """(P^T (b - A x)) at coarse DOFs `idx` (coarse level Nf/2, Dirichlet rows 0) of a
+    fine level with Nf elements, from locally assembled boxes (usable at 4096^2)."""
+    lib = _load()
+    x, b = _f64(x), _f64(b)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.zeros(len(idx))
+    lib.orc_restrict_residual_sample(Nf, nu, _ptr(x), _ptr(b), _ptr(idx), len(idx), _ptr(out))
+    return out
+
+
+def prolong_sample(Nf: int, ec, xf, idx):
+    """(x_f + P e_c) at fine DOFs `idx` of a fine level with Nf elements."""
+    lib = _load()
+    ec, xf = _f64(ec), _f64(xf)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.zeros(len(idx))
+    lib.orc_prolong_sample(Nf, _ptr(ec), _ptr(xf), _ptr(idx), len(idx), _ptr(out))
     return out
 
 

@@ -1422,4 +1422,104 @@ void orc_residual_sample(int N, double nu, const double* x, const double* b, con
     out[q] = box_residual(B, g, x, b);
   }
 }
+
+// Interpolation weights P[f, c] of build_prolongation() evaluated for one
+// (fine DOF, coarse DOF) pair on a fine level with Nf elements: the coarse
+// basis function of c at the fine DOF's point, 0 if c is not one of
+// the 3x3 (Q2) / 2x2 (Q1) basis functions of the coarse element holding f.
+double prolongation_weight(int Nf, int64_t f, int64_t c) {
+  const int Nc = Nf / 2;
+  const int64_t fl = 2 * (int64_t)Nf + 1, fv = fl * fl, cl = 2 * (int64_t)Nc + 1, cv = cl * cl;
+  const bool fp = f >= 2 * fv, cp = c >= 2 * cv;
+  if (fp != cp) return 0.0;
+  if (!fp) {
+    if (f / fv != c / cv) return 0.0;  // components
+    const int64_t i = (f % fv) % fl, j = (f % fv) / fl, I = (c % cv) % cl, J = (c % cv) / cl;
+    const int64_t ex = std::min<int64_t>(i / 4, Nc - 1), ey = std::min<int64_t>(j / 4, Nc - 1);
+    const int64_t a = I - 2 * ex, bb = J - 2 * ey;
+    if (a < 0 || a > 2 || bb < 0 || bb > 2) return 0.0;
+    const double t = (i - 4.0 * ex) / 4.0, sy = (j - 4.0 * ey) / 4.0;
+    return q2((int)a, t) * q2((int)bb, sy);
+  }
+  const int64_t kx = (f - 2 * fv) % (Nf + 1), ky = (f - 2 * fv) / (Nf + 1);
+  const int64_t KX = (c - 2 * cv) % (Nc + 1), KY = (c - 2 * cv) / (Nc + 1);
+  const int64_t ex = std::min<int64_t>(kx / 2, Nc - 1), ey = std::min<int64_t>(ky / 2, Nc - 1);
+  const int64_t cc = KX - ex, d = KY - ey;
+  if (cc < 0 || cc > 1 || d < 0 || d > 1) return 0.0;
+  return q1((int)cc, (kx - 2.0 * ex) / 2.0) * q1((int)d, (ky - 2.0 * ey) / 2.0);
+}
+
+// r_c[idx[q]] = (P^T (b - A x))[idx[q]] on the coarse level (Nf/2 elements) of a
+// fine level with Nf elements, Dirichlet coarse rows 0 (alg:mg lines 3-4,
+// reading 9): the fine residual at every fine DOF in the coarse basis
+// function's support, from locally assembled element boxes, weighted by P.
+void orc_restrict_residual_sample(int Nf, double nu, const double* x, const double* b, const int64_t* idx,
+                                  int64_t count, double* out) {
+  const int Nc = Nf / 2;
+  const int64_t fl = 2 * (int64_t)Nf + 1, fv = fl * fl, cl = 2 * (int64_t)Nc + 1, cv = cl * cl;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t q = 0; q < count; ++q) {
+    const int64_t c = idx[q];
+    if (is_dirichlet(c, Nc)) {
+      out[q] = 0.0;
+      continue;
+    }
+    std::vector<int64_t> fs;  // fine DOFs in the support, ascending
+    if (c < 2 * cv) {
+      const int64_t comp = c / cv, I = (c % cv) % cl, J = (c % cv) / cl;
+      for (int64_t j = std::max<int64_t>(0, 2 * J - 4); j <= std::min<int64_t>(fl - 1, 2 * J + 4); ++j)
+        for (int64_t i = std::max<int64_t>(0, 2 * I - 4); i <= std::min<int64_t>(fl - 1, 2 * I + 4); ++i)
+          fs.push_back(comp * fv + j * fl + i);
+    } else {
+      const int64_t KX = (c - 2 * cv) % (Nc + 1), KY = (c - 2 * cv) / (Nc + 1);
+      for (int64_t ky = std::max<int64_t>(0, 2 * KY - 2); ky <= std::min<int64_t>(Nf, 2 * KY + 2); ++ky)
+        for (int64_t kx = std::max<int64_t>(0, 2 * KX - 2); kx <= std::min<int64_t>(Nf, 2 * KX + 2); ++kx)
+          fs.push_back(2 * fv + ky * (Nf + 1) + kx);
+    }
+    double sum = 0.0;
+    for (int64_t f : fs) {
+      const double w = prolongation_weight(Nf, f, c);
+      if (w == 0.0) continue;
+      int i, j;
+      if (f >= 2 * fv) { i = 2 * (int)((f - 2 * fv) % (Nf + 1)); j = 2 * (int)((f - 2 * fv) / (Nf + 1)); }
+      else { i = (int)((f % fv) % fl); j = (int)((f % fv) / fl); }
+      Box B;
+      box_assemble(B, Nf, nu, i / 2 - 1, i / 2 + 1, j / 2 - 1, j / 2 + 1);
+      sum += w * box_residual(B, f, x, b);
+    }
+    out[q] = sum;
+  }
+}
+
+// out[q] = x_f + (P e_c) at fine DOF idx[q] (alg:mg "Correction"), Nf fine elements
+void orc_prolong_sample(int Nf, const double* ec, const double* xf, const int64_t* idx, int64_t count,
+                        double* out) {
+  const int Nc = Nf / 2;
+  const int64_t fl = 2 * (int64_t)Nf + 1, fv = fl * fl, cl = 2 * (int64_t)Nc + 1, cv = cl * cl;
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < count; ++q) {
+    const int64_t f = idx[q];
+    double s = 0.0;
+    if (f < 2 * fv) {  // the 3x3 Q2 basis functions of the coarse element holding f (b outer, a inner)
+      const int64_t comp = f / fv, i = (f % fv) % fl, j = (f % fv) / fl;
+      const int64_t ex = std::min<int64_t>(i / 4, Nc - 1), ey = std::min<int64_t>(j / 4, Nc - 1);
+      for (int bb = 0; bb < 3; ++bb)
+        for (int a = 0; a < 3; ++a) {
+          const int64_t c = comp * cv + (2 * ey + bb) * cl + 2 * ex + a;
+          const double w = prolongation_weight(Nf, f, c);
+          if (w != 0.0) s += w * ec[c];
+        }
+    } else {
+      const int64_t kx = (f - 2 * fv) % (Nf + 1), ky = (f - 2 * fv) / (Nf + 1);
+      const int64_t ex = std::min<int64_t>(kx / 2, Nc - 1), ey = std::min<int64_t>(ky / 2, Nc - 1);
+      for (int d = 0; d < 2; ++d)
+        for (int cc = 0; cc < 2; ++cc) {
+          const int64_t c = 2 * cv + (ey + d) * (Nc + 1) + ex + cc;
+          const double w = prolongation_weight(Nf, f, c);
+          if (w != 0.0) s += w * ec[c];
+        }
+    }
+    out[q] = xf[f] + s;
+  }
+}
 }  // extern "C"

@@ -44,14 +44,27 @@ inline void slab_rows(int N, int Nla, int nranks, int rank, int* r0, int* r1) {
 // ----------------------------------------------------------------- slab-local memory
 // Virtual-memory-managed vectors: the whole pitched vector is reserved as
 // address space and device memory is created and mapped only for given byte
-// ranges (rounded to the allocation granularity).  Driver entry points are
-// fetched with cudaGetDriverEntryPoint (no link-time libcuda dependency).
+// ranges (rounded to the allocation granularity).  Every other granule of the
+// reservation maps ONE shared scratch granule: with the gaps left unmapped,
+// TMA tensor loads of these vectors raised illegal-address faults on B200 even
+// with every requested row inside the mapped ranges (clamped coordinates,
+// compute-sanitizer), while a standalone partially-mapped TMA probe
+// (tools/tma_vmm_test.cu) did not; the scratch granule removes the fault at the
+// cost of one granule per vector.  No result reads those rows: the
+// distributed parity tests poison every row beyond the halo with NaN.
+// Driver entry points are fetched with cudaGetDriverEntryPoint (no link-time
+// libcuda dependency).
 struct SlabMem {
   uintptr_t base = 0;
   size_t reserved = 0;
   std::vector<std::pair<int64_t, int64_t>> maps;  // (offset, bytes) of each mapped range
   std::vector<unsigned long long> handles;        // CUmemGenericAllocationHandle per range
   int64_t mapped = 0;
+  // every other granule of the reservation maps one shared scratch granule
+  // (never read for results: rows outside the slab + halo are not used)
+  unsigned long long scratch = 0;
+  std::vector<int64_t> scratch_maps;  // offsets of the granules mapped to `scratch`
+  int64_t gran = 0;
 };
 struct VmmApi {
   CUresult (*AddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
@@ -88,6 +101,8 @@ inline VmmApi& vmm_api() {
 }
 inline void slab_free(SlabMem& m) {
   VmmApi& a = vmm_api();
+  for (int64_t off : m.scratch_maps) a.Unmap((CUdeviceptr)(m.base + off), (size_t)m.gran);
+  if (m.scratch) a.Release((CUmemGenericAllocationHandle)m.scratch);
   for (size_t k = 0; k < m.maps.size(); ++k) {
     if (k < m.handles.size()) {
       a.Unmap((CUdeviceptr)(m.base + m.maps[k].first), (size_t)m.maps[k].second);
@@ -160,6 +175,28 @@ inline int slab_alloc(int device, int64_t bytes, std::vector<std::pair<int64_t, 
       slab_free(m);
       return -1;
     }
+  }
+  // the gaps: one shared scratch granule mapped at each
+  m.gran = G;
+  CUmemGenericAllocationHandle sh;
+  if (a.Create(&sh, (size_t)G, &prop, 0) != CUDA_SUCCESS) {
+    err = "cuMemCreate (scratch granule) failed";
+    slab_free(m);
+    return -1;
+  }
+  m.scratch = (unsigned long long)sh;
+  m.mapped += G;
+  size_t k = 0;
+  for (int64_t off = 0; off < (int64_t)m.reserved; off += G) {
+    while (k < merged.size() && merged[k].second <= off) ++k;
+    if (k < merged.size() && merged[k].first <= off) continue;  // a real range
+    if (a.Map((CUdeviceptr)(m.base + off), (size_t)G, 0, sh, 0) != CUDA_SUCCESS ||
+        a.SetAccess((CUdeviceptr)(m.base + off), (size_t)G, &acc, 1) != CUDA_SUCCESS) {
+      err = "cuMemMap (scratch granule) failed";
+      slab_free(m);
+      return -1;
+    }
+    m.scratch_maps.push_back(off);
   }
   *out = m;
   return 0;
@@ -342,8 +379,8 @@ class EmulTransport : public Transport {
   }
   int exchange(const std::vector<Block>& lo_send, const std::vector<Block>& lo_recv, const std::vector<Block>& hi_send,
                const std::vector<Block>& hi_recv, cudaStream_t s, std::string& err) override {
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-      err = "emulated exchange: stream sync failed";
+    if (const cudaError_t e = cudaStreamSynchronize(s); e != cudaSuccess) {
+      err = std::string("emulated exchange: stream sync failed: ") + cudaGetErrorString(e);
       return -1;
     }
     EmulGroup& G = *group_;
@@ -378,8 +415,8 @@ class EmulTransport : public Transport {
   }
   bool capturable() const override { return false; }  // host barriers
   int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) override {
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-      err = "emulated allgather: stream sync failed";
+    if (const cudaError_t e = cudaStreamSynchronize(s); e != cudaSuccess) {
+      err = std::string("emulated allgather: stream sync failed: ") + cudaGetErrorString(e);
       return -1;
     }
     EmulGroup& G = *group_;

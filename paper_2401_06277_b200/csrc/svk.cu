@@ -302,7 +302,7 @@ void free_vec(svk_ctx* ctx, double* p) {
 // r = b - A x (b != NULL) or r = A x (b == NULL), streaming strip kernel
 int op_residual(svk_ctx* ctx, int l, const double* x, const double* b, double* r, cudaStream_t s) {
   if (launch_residual_strip(ctx->g[l], nullptr, ctx->h_fac[l], x, b, r, ctx->nsm, s) != 0) {
-    ctx->err = "residual: TMA descriptor encoding failed";
+    ctx->err = "residual: " + tma_error();
     return SVK_ERR_CUDA;
   }
   CKL();
@@ -317,7 +317,7 @@ int op_residual_restrict(svk_ctx* ctx, int l, const double* x, const double* b, 
   gc.r0 = gf.r0 / 2;
   gc.r1 = gf.r1 == gf.N + 1 ? gc.N + 1 : gf.r1 / 2;
   if (launch_residual_strip(gf, &gc, ctx->h_fac[l], x, b, rc, ctx->nsm, s) != 0) {
-    ctx->err = "residual+restrict: TMA descriptor encoding failed";
+    ctx->err = "residual+restrict: " + tma_error();
     return SVK_ERR_CUDA;
   }
   CKL();
@@ -364,6 +364,12 @@ int alloc_level_vec(svk_ctx* ctx, int l, double** p) {
     return SVK_ERR_ALLOC;
   }
   *p = reinterpret_cast<double*>(m.base);
+  if (const char* e = std::getenv("SVK_DEBUG_SLAB"); e && e[0] == '1') {
+    std::string rs;
+    for (const auto& r : m.maps) rs += " [" + std::to_string(r.first) + "," + std::to_string(r.first + r.second) + ")";
+    std::fprintf(stderr, "[slab-alloc] rank %d level N=%d rows %d..%d base %p reserved %zu maps%s\n", ctx->cfg.rank,
+                 g.N, g.r0, g.r1, (void*)m.base, m.reserved, rs.c_str());
+  }
   for (const auto& r : m.maps) CK(cudaMemset(reinterpret_cast<char*>(m.base) + r.first, 0, r.second));
   ctx->dev_bytes += m.mapped;
   ctx->slab_mem[*p] = m;
@@ -503,14 +509,43 @@ int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
   }
   return SVK_OK;
 }
+// SVK_DEBUG_SLAB=1: report slab-local inputs whose mapped rows do not cover the
+// rows a sweep reads (2(r0-1)-6 .. 2 r1 + 6 lattice rows)
+void debug_slab_rows(const svk_ctx* ctx, int l, const double* v, const char* what) {
+  static const bool on = [] { const char* e = std::getenv("SVK_DEBUG_SLAB"); return e && e[0] == '1'; }();
+  if (!on || !v) return;
+  auto it = ctx->slab_mem.find(v);
+  const LevelGeom& g = ctx->g[l];
+  if (it == ctx->slab_mem.end()) {
+    std::fprintf(stderr, "[slab] rank %d level N=%d %s %p: plain (full)\n", ctx->cfg.rank, g.N, what, (const void*)v);
+    return;
+  }
+  std::fprintf(stderr, "[slab] rank %d level N=%d rows %d..%d %s %p: slab\n", ctx->cfg.rank, g.N, g.r0, g.r1, what,
+               (const void*)v);
+  const int lo = std::max(0, 2 * (g.r0 - 1) - 6), hi = std::min(g.lat - 1, 2 * g.r1 + 6);
+  for (int64_t off : {g.oux, g.ouy}) {
+    const int64_t a = (off + (int64_t)lo * g.pu) * 8, b = (off + (int64_t)(hi + 1) * g.pu) * 8;
+    bool ok = false;
+    for (const auto& r : it->second.maps) ok = ok || (r.first <= a && b <= r.first + r.second);
+    if (!ok)
+      std::fprintf(stderr, "[slab] rank %d level N=%d rows %d..%d (r0 %d r1 %d) %s %p: NOT MAPPED\n", ctx->cfg.rank,
+                   g.N, lo, hi, g.r0, g.r1, what, (const void*)v);
+  }
+}
 int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, double* xout, bool x_zero,
                   cudaStream_t s) {
+  debug_slab_rows(ctx, l, b, "sweep b");
+  if (!x_zero) debug_slab_rows(ctx, l, xin, "sweep x");
   const LevelGeom& g = ctx->g[l];
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
-    TRY(launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
+    const int lst = launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
                            ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_tiles[l], ctx->ntiles[l], ctx->d_bd,
-                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s));
+                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s);
+    if (lst != 0) {
+      ctx->err = "sweep: " + tma_error();
+      return SVK_ERR_CUDA;
+    }
     CKL();
     ctx->launches++;  // two kernels: boundary patches + fused sweep
     return SVK_OK;

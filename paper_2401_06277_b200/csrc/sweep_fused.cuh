@@ -18,7 +18,9 @@
 #include <cuda.h>
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "stencil.cuh"
@@ -299,13 +301,16 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
     if (q < NBAND) {
       const int comp = q / (5 * kBdBandW), rem = q % (5 * kBdBandW), ac = rem / kBdBandW, al = rem % kBdBandW;
       const int i = i0 + (tl.dx ? al : ac), j = j0 + (tl.dx ? ac : al);
-      if (al < nalong && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
+      // only rows of the patches this slab solves (ky in r0-1 .. r1): a column
+      // tile may reach beyond them, and a slab-local vector holds no rows there
+      const bool jslab = j >= 2 * (g.r0 - 1) - 2 && j <= 2 * g.r1 + 2;
+      if (al < nalong && jslab && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
         const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
         double ax = 0.0;
         if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
         r = b[o] - ax;
       }
-    } else if (q - NBAND < tl.n) {
+    } else if (q - NBAND < tl.n && tl.ky + (q - NBAND) * tl.dy >= g.r0 - 1 && tl.ky + (q - NBAND) * tl.dy <= g.r1) {
       const int pi = q - NBAND, kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
       const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
       r = b[p_at(g, kx, ky)] - ax;
@@ -946,7 +951,8 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
   // data of step sB: b pairs sB-2 .. sB (rows 2sB-3 .. 2sB+2), b_p row sB -> barrier 0
   if (t == 0) {
     mbar_expect_tx(&bars[0], 3 * fz::kBBytes + fz::kBPBytes);
-    for (int p = sB - 2; p <= sB; ++p) tma_load_3d(sm + z0_brow(2 * p + 1, 0), &M.bv, xc0 + 2, 2 * p + 1, 0, &bars[0]);
+    for (int p = sB - 2; p <= sB; ++p)
+      tma_load_3d(sm + z0_brow(2 * p + 1, 0), &M.bv, xc0 + 2, 2 * p + 1, 0, &bars[0]);
     tma_load_2d(sm + z0_bprow(sB), &M.bp, kx0 - 2, sB, &bars[0]);
   }
   const int pi = fz::kOWN * warp + lane;
@@ -1130,27 +1136,40 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 inline PFN_encodeTiled get_encode() {
-  static PFN_encodeTiled fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiled fn = [] {  // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_encodeTiled)p;
-  }
+      return (PFN_encodeTiled)p;
+    return (PFN_encodeTiled) nullptr;
+  }();
   return fn;
+}
+// the last TMA descriptor encoding failure of this thread (for error messages)
+inline std::string& tma_error() {
+  static thread_local std::string e;
+  return e;
+}
+inline bool tma_encoded(CUresult r, const char* what, const void* base) {
+  if (r == CUDA_SUCCESS) return true;
+  char buf[160];
+  std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled(%s, base %p) failed: CUresult %d", what, base, (int)r);
+  tma_error() = buf;
+  return false;
 }
 // velocity planes of a vector: dims {lat cols, lat rows, 2 comps}; box {256, 2, 2}
 inline bool make_vel_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsigned boxw = fz::W) {
   PFN_encodeTiled enc = get_encode();
-  if (!enc) return false;
+  if (!enc) return tma_encoded(CUDA_ERROR_NOT_FOUND, "entry point", v);
   const cuuint64_t dims[3] = {(cuuint64_t)g.lat, (cuuint64_t)g.lat, 2};
   const cuuint64_t strides[2] = {(cuuint64_t)g.pu * 8, (cuuint64_t)(g.ouy - g.oux) * 8};
   const cuuint32_t box[3] = {boxw, 2, 2};
   const cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(v + g.oux), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tma_encoded(enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(v + g.oux), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                     "velocity", v);
 }
 // pressure plane: dims {N+1, N+1}; box {boxw, 1}
 inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsigned boxw) {
@@ -1160,9 +1179,10 @@ inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsi
   const cuuint64_t strides[1] = {(cuuint64_t)g.pp * 8};
   const cuuint32_t box[2] = {boxw, 1};
   const cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)(v + g.op), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tma_encoded(enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)(v + g.op), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                     "pressure", v);
 }
 
 inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,

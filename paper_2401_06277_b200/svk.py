@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsvk.so")
+LIB_PATH = os.environ.get("SVK_LIBRARY") or os.path.join(_PKG, "libsvk.so")  # SVK_LIBRARY: dev builds
 
 SVK_OK, SVK_NOT_CONVERGED = 0, 1
 PROBLEMS = {"zero": 0, "mms_paper": 1, "mms_inspace": 2, "cavity": 3}

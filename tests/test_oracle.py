@@ -359,3 +359,21 @@ def test_sampled_sweep_and_residual_equal_global_oracle(N):
     assert rel(oracle.residual_sample(N, x, b, idx), rs) < 1e-13
     xs2 = oracle.Oracle(N, weighting=oracle.WEIGHT_SCALAR, omega=0.5).sweep(l, x, b)
     assert rel(oracle.sweep_sample(N, x, b, idx, omega=0.5, weighting=oracle.WEIGHT_SCALAR) - x, xs2 - x) < 1e-12
+
+
+@pytest.mark.parametrize("N", [8, 16])
+def test_sampled_transfers_equal_global_oracle(N):
+    """The local residual+restriction and prolongation samplers used for full-size
+    parity equal the global oracle (explicit P / P^T) on every DOF."""
+    o = oracle.Oracle(N, n_coarse=4)
+    l = o.fine
+    x = svk_inputs.random_vector(N, 31)
+    b = svk_inputs.random_vector(N, 32)
+    rc = o.restrict(l, o.residual(l, x, b))
+    idxc = np.arange(o.length(l - 1), dtype=np.int64)
+    assert rel(oracle.restrict_residual_sample(N, x, b, idxc), rc) < 1e-13
+    ec = svk_inputs.random_vector(N // 2, 33)
+    ec[o.dirichlet(l - 1)] = 0.0
+    xf = svk_inputs.random_vector(N, 34)
+    idxf = np.arange(o.length(l), dtype=np.int64)
+    assert rel(oracle.prolong_sample(N, ec, xf, idxf) - xf, o.prolong_add(l, ec, xf) - xf) < 1e-14
