@@ -391,6 +391,63 @@ def run_svk(args):
     return 0
 
 
+def run_emulated(args):
+    """--emulate: args.gpus logical ranks in threads on cuda:0 through the EMULATED
+    transport (row slabs, halo exchanges, agglomeration all-gather, all-reduced
+    dots; only the byte mover differs from NCCL).  A logic check of the
+    multi-GPU path at full size, not a multi-GPU measurement."""
+    import threading
+    import torch
+    from paper_2401_06277_b200 import Solver
+    P, N = args.gpus, args.n
+    Ss = [Solver(N, rank=r, nranks=P, transport="emulated", agglom_rows=args.agglom, emul_group=4242)
+          for r in range(P)]
+    res, errs = [None] * P, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                S = Ss[r]
+                b, x0 = S.set_problem("mms_paper")
+                x = S.new_vector()
+                for _ in range(args.warmup):
+                    x.copy_(x0)
+                    S.fgmres(b, x, rtol=args.rtol, maxit=args.maxit)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                its = []
+                for _ in range(args.steps):
+                    x.copy_(x0)
+                    rep, _ = S.fgmres(b, x, rtol=args.rtol, maxit=args.maxit)
+                    its.append(rep["iterations"])
+                e1.record(st)
+                st.synchronize()
+                res[r] = (e0.elapsed_time(e1) / 1e3, its, rep["rel_residual"], S.device_bytes)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    t = max(q[0] for q in res)
+    line = {"metric": METRIC, "value": n_dof(N) * args.steps / t, "unit": "DOF/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper manufactured solution, P:76-81)",
+            "emulated": "%d logical ranks on one GPU (emulated transport): a logic check of the slab path, "
+                        "not a multi-GPU measurement" % P,
+            "config": dict(config_dict(args, P), parallelism="slabs%d-emulated" % P),
+            "iterations": res[0][1][-1], "iterations_per_rank": [q[1][-1] for q in res],
+            "rel_residual": res[0][2], "device_bytes_per_rank": [q[3] for q in res]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,6 +467,8 @@ def main():
     ap.add_argument("--ref-n", type=int, default=512)
     ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs")
     ap.add_argument("--agglom", type=int, default=64)
+    ap.add_argument("--emulate", action="store_true",
+                    help="--gpus N logical ranks on one GPU through the emulated transport (logic check)")
     ap.add_argument("--relax", choices=["vanka", "bs", "su"], default="vanka",
                     help="V-cycle relaxation; bs / su are the paper's same-run comparators (configs[4], 1 GPU)")
     ap.add_argument("--precond", choices=["mg", "bt"], default="mg",
@@ -421,6 +480,8 @@ def main():
         ap.error("--relax bs/su: single-GPU comparator runs of the svk arm only")
     if args.warmup < 3:
         args.warmup = 3
+    if args.emulate:
+        return run_emulated(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: relaunch this script under torchrun (the driver's own launch sets WORLD_SIZE)
         import socket
