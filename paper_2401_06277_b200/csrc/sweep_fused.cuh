@@ -871,6 +871,15 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
     //      and x_out on rows 2s-2, 2s-1 (node row s-1), which are now complete ----
     const int ny = s - 1;
     const bool rowout = colout && ny >= y0 && ny < y1;  // the row test is uniform over the CTA
+    // x_in of the output rows, loaded ahead of the shuffles (hides the shared-memory latency)
+    double2 xin_o[2][2];  // [component][row parity]
+    if (rowout) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) xin_o[c][rr] = lds2(sm + S.xr(rr - 2, c) + 2 * pi + 4);
+    }
+    double* const ou_row = out_u + (int64_t)(2 * ny) * g.pu;  // dereferenced only when rowout
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const double* v = c ? vy : vx;
@@ -889,13 +898,13 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_fused(const FusedA
         carry[r][c][1] = S1[r + 2];
       }
       if (rowout) {
-        double* const oc = (c ? out_v : out_u) + (int64_t)(2 * ny) * g.pu;
+        double* const oc = ou_row + (c ? g.ouy - g.oux : 0);
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int j = 2 * ny + rr;  // rr = row parity
           if (j > lat - 1) continue;  // uniform: the row past the last lattice row
           const bool jin = j >= 1 && j <= lat - 2;  // uniform: Dirichlet rows keep x_in
-          const double2 x = lds2(sm + S.xr(rr - 2, c) + 2 * pi + 4);
+          const double2 x = xin_o[c][rr];
           const double w0 = jin ? wgt[rr][0] : 0.0, w1 = jin ? wgt[rr][1] : 0.0;
           *reinterpret_cast<double2*>(oc + rr * g.pu) = make_double2(fma(w0, S0[rr], x.x), fma(w1, S1[rr], x.y));
         }
@@ -965,12 +974,16 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
     for (int c = 0; c < 2; ++c) carry[r][c][0] = carry[r][c][1] = 0.0;
   const int i0 = 2 * kxp;
   const bool cin0 = i0 >= 1 && i0 <= lat - 2, cin1 = i0 + 1 <= lat - 2;
-  double wgt[2][2];  // [row parity][column parity], as in k_vanka_fused
+  double wgt[2][2];  // [row parity][column parity], column mask folded in (as k_vanka_fused)
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
-      wgt[a][b] = A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0);
+      wgt[a][b] = (b ? cin1 : cin0)
+                      ? (A.scalar_w ? A.omega : A.omega * (a ? 0.5 : 1.0 / 3.0) * (b ? 0.5 : 1.0 / 3.0))
+                      : 0.0;
+  const bool colout = owner && 2 * kxp < g.pu;
+  double* const out_u = A.xout + g.oux + i0;  // dereferenced only when colout
   for (int s = sB; s <= sE; ++s) {
     // step s: b pair s and b_p row s arrived on barrier (s-sB)&1.  After the CTA
     // barrier every thread has finished step s-1 (windows of pairs s-3 .. s-1),
@@ -1019,7 +1032,8 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
     if (owner && s >= y0 && s < y1 && kxp < g.pp)
       A.xout[g.op + (int64_t)s * g.pp + kxp] = kxp <= N ? A.omega * dp : 0.0;
     const int ny = s - 1;
-    const bool rowout = owner && ny >= y0 && ny < y1 && 2 * kxp < g.pu;
+    const bool rowout = colout && ny >= y0 && ny < y1;  // the row test is uniform over the CTA
+    double* const ou_row = out_u + (int64_t)(2 * ny) * g.pu;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const double* v = c ? vy : vx;
@@ -1038,13 +1052,14 @@ __global__ void __launch_bounds__(fz::kNT, fz::kMinB) k_vanka_zero(const FusedAr
         carry[r][c][1] = S1[r + 2];
       }
       if (rowout) {
+        double* const oc = ou_row + (c ? g.ouy - g.oux : 0);
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int j = 2 * ny + rr;
-          if (j > lat - 1) continue;
-          const bool jin = j >= 1 && j <= lat - 2;
-          *reinterpret_cast<double2*>(A.xout + (c ? g.ouy : g.oux) + (int64_t)j * g.pu + i0) =
-              make_double2((jin && cin0) ? wgt[rr][0] * S0[rr] : 0.0, (jin && cin1) ? wgt[rr][1] * S1[rr] : 0.0);
+          if (j > lat - 1) continue;                // uniform
+          const bool jin = j >= 1 && j <= lat - 2;  // uniform: Dirichlet rows are 0
+          const double w0 = jin ? wgt[rr][0] : 0.0, w1 = jin ? wgt[rr][1] : 0.0;
+          *reinterpret_cast<double2*>(oc + rr * g.pu) = make_double2(w0 * S0[rr], w1 * S1[rr]);
         }
       }
     }
