@@ -262,6 +262,17 @@ int svk_vanka_sweep(svk_ctx* ctx, int32_t level, const double* x_in, const doubl
  * `level` is the FINE level (>= 1). */
 int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_coarse, void* stream);
 
+/* Residual and restriction in one pass (alg:mg lines 3-4; the
+ * V-cycle's own kernel, k_residual_strip<MODE 1>): r_coarse = P^T (b - A x) on
+ * level-1, Dirichlet rows 0 (reading 9); the fine residual never reaches
+ * memory.  x, b: level `level` vectors; r_coarse: level `level`-1 vector, must
+ * not alias them.  Asynchronous on `stream`.  Multi-GPU: halos of x and b are
+ * refreshed; on the agglomeration level the coarse vector is assembled on every
+ * rank (all-gather), on a distributed coarse level only the rank's rows are
+ * written.  SVK_ERR_INVALID on level < 1, bad pointers or aliasing. */
+int svk_residual_restrict(svk_ctx* ctx, int32_t level, const double* x, const double* b, double* r_coarse,
+                          void* stream);
+
 /* x_fine += P e_coarse (alg:mg line 9).  `level` is the FINE level. */
 int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double* x_fine, void* stream);
 

@@ -1689,6 +1689,27 @@ int svk_restrict(svk_ctx* ctx, int32_t level, const double* r_fine, double* r_co
   });
 }
 
+int svk_residual_restrict(svk_ctx* ctx, int32_t level, const double* x, const double* b, double* r_coarse,
+                          void* stream) {
+  return guarded(ctx, [&]() -> int {
+    TRY(valid_level(ctx, level));
+    if (level < 1) return SVK_ERR_INVALID;
+    TRY(valid_ptr(ctx, x, "x"));
+    TRY(valid_ptr(ctx, b, "b"));
+    TRY(valid_ptr(ctx, r_coarse, "r_coarse"));
+    if (r_coarse == x || r_coarse == b) {
+      ctx->err = "r_coarse aliases an input";
+      return SVK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(op_halo(ctx, level, const_cast<double*>(x), s));
+    TRY(op_halo(ctx, level, const_cast<double*>(b), s));
+    TRY(op_residual_restrict(ctx, level, x, b, r_coarse, s));
+    if (dist_level(ctx, level) && !dist_level(ctx, level - 1)) TRY(op_agglomerate(ctx, level, r_coarse, s));
+    return SVK_OK;
+  });
+}
+
 int svk_prolong_add(svk_ctx* ctx, int32_t level, const double* e_coarse, double* x_fine, void* stream) {
   return guarded(ctx, [&]() -> int {
     TRY(valid_level(ctx, level));

@@ -77,6 +77,7 @@ EXPORTS = {
     "svk_precond_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_prolong_add": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "svk_residual_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_coarse_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_vcycle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "svk_fgmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
@@ -316,6 +317,13 @@ class Solver:
         out = self.new_vector(level - 1) if out is None else out
         self._chk(self.lib.svk_restrict(self._h, level, self._vec(rf, level, "r_fine"),
                                         self._vec(out, level - 1, "r_coarse"), self._stream()))
+        return out
+
+    def residual_restrict(self, level, x, b, out=None):
+        """r_c = P^T (b - A x) on level-1 in one pass (svk_residual_restrict)."""
+        out = self.new_vector(level - 1) if out is None else out
+        self._chk(self.lib.svk_residual_restrict(self._h, level, self._vec(x, level, "x"), self._vec(b, level, "b"),
+                                                 self._vec(out, level - 1, "r_coarse"), self._stream()))
         return out
 
     def prolong_add(self, level, ec, xf):

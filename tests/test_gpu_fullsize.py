@@ -55,6 +55,32 @@ def test_fullsize_sweep_and_residual_sampled(solver):
     assert np.abs(rg[idx] - ro).max() <= 1e-13 * np.abs(ro).max()
 
 
+def test_fullsize_residual_restrict_and_prolong_sampled(solver):
+    """The transfer kernels at 4096^2 in the V-cycle's launch configuration:
+    r_c = P^T (b - A x) (fused residual + restriction) sampled on the 2048^2
+    level, and x_f + P e_c sampled on the fine level, against the oracle's local
+    samplers (oracle.restrict_residual_sample / prolong_sample)."""
+    S = solver
+    Nc = N // 2
+    x = svk_inputs.random_vector(N, 111)
+    b = svk_inputs.random_vector(N, 112)
+    rc = S.to_compact(S.residual_restrict(S.fine, S.from_compact(x), S.from_compact(b)), S.fine - 1).cpu().numpy()
+    idxc = np.union1d(svk_inputs.random_sample_indices(Nc, 113, 400), structured_samples(Nc))
+    ro = oracle.restrict_residual_sample(N, x, b, idxc)
+    assert np.abs(rc[idxc] - ro).max() <= 1e-12 * np.abs(ro).max()
+    del rc
+    ec = svk_inputs.random_vector(Nc, 114)
+    latc = 2 * Nc + 1
+    for comp in range(2):  # coarse Dirichlet entries of a correction are 0
+        pl = ec[comp * latc * latc:(comp + 1) * latc * latc].reshape(latc, latc)
+        pl[0, :] = pl[-1, :] = pl[:, 0] = pl[:, -1] = 0.0
+    xg = S.to_compact(S.prolong_add(S.fine, S.from_compact(ec, S.fine - 1), S.from_compact(x)), S.fine).cpu().numpy()
+    idx = np.union1d(svk_inputs.random_sample_indices(N, 115, 400), structured_samples(N))
+    po = oracle.prolong_sample(N, ec, x, idx)
+    d_g, d_o = xg[idx] - x[idx], po - x[idx]
+    assert np.abs(d_g - d_o).max() <= 1e-13 * np.abs(d_o).max()
+
+
 def test_fullsize_mms_nodal_exactness(solver):
     S = solver
     b, x = S.set_problem("mms_paper")

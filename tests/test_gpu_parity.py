@@ -109,6 +109,19 @@ def test_transfer_parity(gpu, N):
         assert rel(out - xf, ref - xf) < 1e-13
 
 
+@pytest.mark.parametrize("N", [16, 64, 256])
+def test_residual_restrict_parity(gpu, N):
+    """The V-cycle's fused residual + restriction (svk_residual_restrict) on every
+    level against the oracle's explicit P^T (b - A x)."""
+    S, O = get_solver(N), get_oracle(N)
+    for l in range(1, S.levels):
+        n = S.info[l].N
+        x = svk_inputs.random_vector(n, 41)
+        b = svk_inputs.random_vector(n, 42)
+        rc = to_np(S, S.residual_restrict(l, S.from_compact(x, l), S.from_compact(b, l)), l - 1)
+        assert rel(rc, O.restrict(l, O.residual(l, x, b))) < 1e-13, l
+
+
 def test_coarse_solve_parity(gpu):
     S, O = get_solver(16), get_oracle(16)
     for seed in (1, 2, 3):
