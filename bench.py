@@ -214,7 +214,23 @@ def cpu_baseline(args):
         _, its, _, _, _ = o.fgmres(b, x0, rtol=args.rtol)
         t += time.perf_counter() - t0
         nsolve += 1
+    # context: the oracle's one full-size solve, recorded by tests/test_gpu_iterations_large.py
+    # (SVK_LARGE_ORACLE=4096) on a GPU box's 16 host cores -- not re-timed in this run
+    at_size = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_iteration_parity.jsonl")) as f:
+            for ln in f:
+                if ln.startswith("{"):
+                    r = json.loads(ln)
+                    if r["N"] == args.n and r["kind"] == "mms_paper":
+                        at_size = {"N": r["N"], "solve_s": r["solve_s"], "setup_s": r["setup_s"],
+                                   "dof_per_s": n_dof(r["N"]) / r["solve_s"], "cores": r["threads"],
+                                   "iterations": r["iterations"],
+                                   "source": "profiles/r2_iteration_parity.jsonl (recorded run, not re-timed here)"}
+    except (OSError, ValueError, KeyError):
+        pass
     return {"value": nsolve * n_dof(N) / t, "unit": "DOF/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "oracle_at_benched_size": at_size,
             "sample": "%d FGMRES+V(1,1)-Vanka solve(s) of the %d^2 MMS problem to %g (%d iterations each, %.1f s "
                       "in total; oracle C++/OpenMP, setup excluded)" % (nsolve, N, args.rtol, its, t)}
 
