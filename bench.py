@@ -194,6 +194,8 @@ def config_dict(args, world=1, n=None):
     else:
         wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-%s"
               % (args.n, args.n, RELAX_NAMES[relax]))
+    if getattr(args, "low_memory", False):
+        wl += " (low-memory Krylov: V only, x = x0 + M sum y_j V_j)"
     return {"workload": wl, "relaxation": relax,
             "N": args.n, "levels_to": 4, "dofs": n_dof(args.n), "omega_v": 0.8, "weighting": "multiplicity",
             "sweep_impl": args.sweep, "l2": "inputs exceed L2 (%.2f GB per vector vs 126 MB L2)"
@@ -255,9 +257,10 @@ def run_svk(args):
         from paper_2401_06277_b200 import svk
         nid = svk.nccl_id_broadcast()
         S = Solver(N, sweep=args.sweep, device=dev, rank=rank, nranks=world, transport="nccl",
-                   agglom_rows=args.agglom, nccl_id=nid)
+                   agglom_rows=args.agglom, nccl_id=nid, low_memory=args.low_memory)
     else:
-        S = Solver(N, sweep=args.sweep, device=dev, relax=args.relax, precond=args.precond)
+        S = Solver(N, sweep=args.sweep, device=dev, relax=args.relax, precond=args.precond,
+                   low_memory=args.low_memory)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     b, x0 = S.set_problem("mms_paper")
@@ -483,6 +486,9 @@ def main():
     ap.add_argument("--ref-n", type=int, default=512)
     ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs")
     ap.add_argument("--agglom", type=int, default=64)
+    ap.add_argument("--low-memory", action="store_true",
+                    help="keep only the Arnoldi basis V (right-preconditioned GMRES with the fixed V-cycle, one "
+                         "extra V-cycle at the end): halves the Krylov memory, e.g. 8192^2 on one B200")
     ap.add_argument("--emulate", action="store_true",
                     help="--gpus N logical ranks on one GPU through the emulated transport (logic check)")
     ap.add_argument("--relax", choices=["vanka", "bs", "su"], default="vanka",

@@ -156,6 +156,15 @@ typedef struct svk_config {
                             checks it against its group (svk_validate_patches); default 0 */
   double bt_omega_u;     /* BLOCK_TRIANGULAR: Jacobi weight on L; default 1.0 */
   double bt_omega_p;     /* BLOCK_TRIANGULAR: Jacobi weight on M; default 0.6 */
+  int32_t krylov_store_z; /* 1 (default): FGMRES keeps Z_j = M V_j;
+                             0: low-memory mode for the MG preconditioner, whose V-cycle
+                             from zero is a FIXED linear operator M -- only V_j is kept,
+                             each z_j lives in one buffer until A z_j is formed, and the
+                             update is x = x0 + M (sum_j y_j V_j) with one extra V-cycle:
+                             the same iterates as FGMRES up to rounding (right-
+                             preconditioned GMRES), half the Krylov memory (8192^2 fits
+                             one B200).  Not with BLOCK_TRIANGULAR (kept as FGMRES). */
+  int32_t reserved0;
 } svk_config;
 
 /* FGMRES preconditioner:

@@ -1053,6 +1053,8 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
     return SVK_ERR_NONFINITE;
   }
   int status = SVK_OK, k = 0, n_reorth = 0;
+  // low-memory mode: one z buffer (only with the fixed-linear MG preconditioner)
+  const bool store_z = ctx->cfg.krylov_store_z != 0 || ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR;
   std::vector<const double*> dlist;
   bool conv = beta == 0.0;
   std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), gv(maxit + 1, 0.0), nv(maxit + 2);
@@ -1064,20 +1066,21 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
     inv_nsq[0] = 1.0 / (beta * beta);
     for (int j = 0; j < maxit; ++j) {
       const int m = j + 1;
-      TRY(ensure_vec(ctx->Z, j));
+      TRY(ensure_vec(ctx->Z, store_z ? j : 0));
       TRY(ensure_vec(ctx->V, j + 1));
+      double* const zj = ctx->Z[store_z ? j : 0];
       // basis pointers and scales for this iteration (small H2D copies, stream ordered)
       std::memcpy(ctx->h_pin, inv_nsq.data(), m * sizeof(double));
       CK(cudaMemcpyAsync(ctx->d_coef + oinv, ctx->h_pin, m * sizeof(double), cudaMemcpyHostToDevice, s));
       const double* const* hV = (const double* const*)ctx->V.data();
       // z~_j = M V~_j : one V-cycle from zero
       CK(cudaEventRecord(ctx->ev[0], s));
-      if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) TRY(op_bt(ctx, ctx->V[j], ctx->Z[j], s));
-      else TRY(op_precond_mg(ctx, ctx->V[j], ctx->Z[j], s));
+      if (ctx->cfg.precond == SVK_PRECOND_BLOCK_TRIANGULAR) TRY(op_bt(ctx, ctx->V[j], zj, s));
+      else TRY(op_precond_mg(ctx, ctx->V[j], zj, s));
       CK(cudaEventRecord(ctx->ev[1], s));
       // w~ = A z~_j ; classical Gram-Schmidt pass against V~_0..V~_j (its dot
       // pass also yields |w~|^2) ; V~_j+1 = w~' with |w~'|
-      TRY(op_residual(ctx, L, ctx->Z[j], nullptr, ctx->d_w, s));
+      TRY(op_residual(ctx, L, zj, nullptr, ctx->d_w, s));
       dlist.assign(hV, hV + m);
       dlist.push_back(ctx->d_w);
       TRY(cgs_dots(ctx, dlist.data(), m + 1, ctx->d_w, S, oraw, s));
@@ -1152,10 +1155,27 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       }
       for (int i = 0; i < k; ++i) ctx->h_pin[i] = -y[i] / nv[i];
       CK(cudaMemcpyAsync(ctx->d_coef + o1, ctx->h_pin, k * sizeof(double), cudaMemcpyHostToDevice, s));
-      for (int c0 = 0; c0 < k; c0 += kCgsMax) {
-        const int mm = std::min(kCgsMax, k - c0);
-        k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist((const double* const*)ctx->Z.data() + c0, mm), mm,
-                                                         ctx->d_coef + o1 + c0, x, x, S, ctx->d_part);
+      if (store_z) {
+        for (int c0 = 0; c0 < k; c0 += kCgsMax) {
+          const int mm = std::min(kCgsMax, k - c0);
+          k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist((const double* const*)ctx->Z.data() + c0, mm), mm,
+                                                           ctx->d_coef + o1 + c0, x, x, S, ctx->d_part);
+          CKL();
+        }
+      } else {  // x += M (sum_i (y_i / n_i) V~_i): u in d_w (w_out = 0 - sum c_i V~_i), then one V-cycle
+        TRY(op_zero_level(ctx, L, ctx->d_w, s));
+        for (int c0 = 0; c0 < k; c0 += kCgsMax) {
+          const int mm = std::min(kCgsMax, k - c0);
+          k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist((const double* const*)ctx->V.data() + c0, mm), mm,
+                                                           ctx->d_coef + o1 + c0, ctx->d_w, ctx->d_w, S, ctx->d_part);
+          CKL();
+        }
+        TRY(op_halo(ctx, L, ctx->d_w, s));
+        TRY(op_precond_mg(ctx, ctx->d_w, ctx->Z[0], s));
+        ctx->h_pin[0] = -1.0;
+        CK(cudaMemcpyAsync(ctx->d_coef + o1, ctx->h_pin, sizeof(double), cudaMemcpyHostToDevice, s));
+        const double* zl[1] = {ctx->Z[0]};
+        k_cgs_update<<<kDotBlocks, kRedThreads, 0, s>>>(veclist(zl, 1), 1, ctx->d_coef + o1, x, x, S, ctx->d_part);
         CKL();
       }
     }
@@ -1499,6 +1519,7 @@ int svk_config_default(svk_config* cfg, int32_t n_elem) {
   cfg->bt_nu = 3;
   cfg->bt_omega_u = 1.0;
   cfg->bt_omega_p = 0.6;
+  cfg->krylov_store_z = 1;
   return SVK_OK;
 }
 

@@ -41,7 +41,8 @@ class Config(C.Structure):
                 ("orth", C.c_int32), ("relax", C.c_int32), ("jacobi_sweeps", C.c_int32), ("nccl_id", C.c_uint8 * 128),
                 ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double),
                 ("precond", C.c_int32), ("bt_cycles", C.c_int32), ("bt_nu", C.c_int32), ("validate", C.c_int32),
-                ("bt_omega_u", C.c_double), ("bt_omega_p", C.c_double)]
+                ("bt_omega_u", C.c_double), ("bt_omega_p", C.c_double), ("krylov_store_z", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 class LevelInfo(C.Structure):
@@ -157,7 +158,8 @@ class Solver:
                  orth: str = "adaptive", relax: str = "vanka", relax_t: float | None = None,
                  relax_omega: float | None = None, jacobi_omega: float | None = None,
                  jacobi_sweeps: int | None = None, precond: str = "mg", bt_cycles: int = 3, bt_nu: int = 3,
-                 bt_omega_u: float = 1.0, bt_omega_p: float = 0.6, validate: bool = False):
+                 bt_omega_u: float = 1.0, bt_omega_p: float = 0.6, validate: bool = False,
+                 low_memory: bool = False):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
         "emulated" runs nranks logical ranks of one process on one device (one thread each).
@@ -179,6 +181,7 @@ class Solver:
         cfg.precond, cfg.bt_cycles, cfg.bt_nu = PRECOND[precond], bt_cycles, bt_nu
         cfg.bt_omega_u, cfg.bt_omega_p = bt_omega_u, bt_omega_p
         cfg.validate = 1 if validate else 0
+        cfg.krylov_store_z = 0 if low_memory else 1
         if relax != "vanka":
             d = RELAX_DEFAULTS[relax]
             cfg.relax_t = d[0] if relax_t is None else relax_t

@@ -299,3 +299,31 @@ def test_host_arrays_and_arguments_are_checked(gpu):
     for rtol, maxit in ((1e-10, 0), (1e-10, -5), (float("nan"), 10), (-1.0, 10)):
         assert S.lib.svk_solve_host(S._h, p, p, q, rtol, maxit, C.byref(rep), None) < 0
     assert S.lib.svk_solve_host(S._h, p, p, p, 1e-10, 10, C.byref(rep), None) < 0
+
+
+@pytest.mark.parametrize("N,kind", [(64, "mms_paper"), (256, "cavity")])
+def test_low_memory_krylov_matches_fgmres(gpu, N, kind):
+    """krylov_store_z = 0 (right-preconditioned GMRES with the fixed V-cycle, one
+    z buffer, x = x0 + M sum y_j V_j): the same iterates as FGMRES up to rounding,
+    so the oracle's iteration count and solution, with half the Krylov memory."""
+    from paper_2401_06277_b200 import Solver
+    O = get_oracle(N)
+    kcode = {"mms_paper": oracle.MMS_PAPER, "cavity": oracle.CAVITY}[kind]
+    bo, x0o = O.problem(kcode)
+    xo, its, ho, _, _ = O.fgmres(bo, x0o, rtol=1e-10, maxit=100)
+    out = {}
+    for low in (False, True):
+        S = Solver(N, low_memory=low)
+        b, x = S.set_problem(kind)
+        rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=100)
+        out[low] = (rep, hist, to_np(S, x, S.fine), S.device_bytes)
+        S.close()
+    (r0, h0, x0g, m0), (r1, h1, x1g, m1) = out[False], out[True]
+    assert r1["converged"] == 1 and r1["iterations"] == r0["iterations"] and abs(r1["iterations"] - its) <= 1
+    assert np.all(np.abs(h1 - h0) <= 1e-9 * np.maximum(h0, 1e-12))
+    assert r1["rel_residual"] < 1e-9
+    nv = (2 * N + 1) ** 2
+    scale = max(np.abs(xo[:2 * nv]).max(), 1.0)
+    assert np.abs(x1g[:2 * nv] - xo[:2 * nv]).max() < 1e-8 * scale
+    assert np.abs(x1g[:2 * nv] - x0g[:2 * nv]).max() < 1e-9 * scale
+    assert m1 < m0
