@@ -190,7 +190,8 @@ def config_dict(args, world=1, n=None):
               "preconditioner (3 V(3,3) Jacobi cycles per block)" % (args.n, args.n))
         relax = "block-triangular"
     elif relax == "vanka":
-        wl = "configs[2]: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka" % (args.n, args.n)
+        tag = {4096: "configs[2]: ", 8192: "configs[3] size: "}.get(args.n, "")
+        wl = "%s2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-Vanka" % (tag, args.n, args.n)
     else:
         wl = ("configs[4] comparator: 2D Stokes Q2-Q1, %dx%d structured mesh, paper MMS, FGMRES(1e-10)+V(1,1)-%s"
               % (args.n, args.n, RELAX_NAMES[relax]))
