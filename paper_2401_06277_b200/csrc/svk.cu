@@ -540,8 +540,8 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
     const int lst = launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
-                           ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_tiles[l], ctx->ntiles[l], ctx->d_bd,
-                           x_zero ? nullptr : xin, b, xout, ctx->nsm, s);
+                                       ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_tiles[l], ctx->ntiles[l],
+                                       ctx->d_bd, x_zero ? nullptr : xin, b, xout, ctx->nsm, s);
     if (lst != 0) {
       ctx->err = "sweep: " + tma_error();
       return SVK_ERR_CUDA;

@@ -506,8 +506,7 @@ struct ResWin {
 };
 // load x window rows R0..R1 and p window rows P0..P1 of step sp
 template <int R0, int R1, int P0, int P1, class RG>
-__device__ __forceinline__ void load_res_win(const double* sm, const RG& rg, int sp, ResWin& w) {
-  const int t = threadIdx.x;
+__device__ __forceinline__ void load_res_win(const double* sm, const RG& rg, int sp, ResWin& w, int t) {
 #pragma unroll
   for (int r = R0; r <= R1; ++r) {
     const double* xu = sm + rg.x(2 * sp + r, 0) + 2 * t;
@@ -522,6 +521,10 @@ __device__ __forceinline__ void load_res_win(const double* sm, const RG& rg, int
 #pragma unroll
     for (int q = 0; q < 3; ++q) w.Pm[r][q] = pr[q];
   }
+}
+template <int R0, int R1, int P0, int P1, class RG>
+__device__ __forceinline__ void load_res_win(const double* sm, const RG& rg, int sp, ResWin& w) {
+  load_res_win<R0, R1, P0, P1, RG>(sm, rg, sp, w, (int)threadIdx.x);
 }
 // step sp -> sp+1 with the overlapping rows kept in registers (x rows 2..4 -> 0..2, p rows 1..2 -> 0..1)
 __device__ __forceinline__ void roll_res_win(ResWin& w) {
@@ -539,8 +542,10 @@ __device__ __forceinline__ void roll_res_win(ResWin& w) {
 }
 template <bool XZERO, bool NOB = false, class RG = RingFz, bool MASK = true>
 __device__ __forceinline__ ResVals residual_from_win(const double* sm, const LevelGeom& g, const FusedFactors& F,
-                                                     int sp, int kx0, const RG& rg, const ResWin& w) {
-  const int N = g.N, lat = g.lat, t = threadIdx.x;
+                                                     int sp, int kx0, const RG& rg, const ResWin& w,
+                                                     int t = -1) {
+  if (t < 0) t = threadIdx.x;
+  const int N = g.N, lat = g.lat;
   const int c0 = 2 * kx0 - 4 + 2 * t;
   const int j0 = 2 * sp + 1, j1 = 2 * sp + 2;
   const bool c0ok = c0 >= 1 && c0 <= lat - 2, c1ok = c0 + 1 >= 1 && c0 + 1 <= lat - 2;
