@@ -44,6 +44,7 @@ struct RingRz {
     return rz_bpair((j - 1) >> 1) + c * 2 * fz::W + ((j - 1) & 1) * fz::W;
   }
   static __device__ __forceinline__ int bp(int r) { return rz::OBP + (r & 3) * fz::PWID; }
+  SVK_RING_B_FROM_SMEM
 };
 
 // the same ring with the x-pair slots of step sp advanced incrementally (RingFzS)
@@ -54,6 +55,7 @@ struct RingRzStep {
   __device__ __forceinline__ int p(int r) const { return rz_prow(r); }
   __device__ __forceinline__ int b(int j, int c) const { return RingRz::b(j, c); }
   __device__ __forceinline__ int bp(int r) const { return RingRz::bp(r); }
+  SVK_RING_B_FROM_SMEM
 };
 
 struct ResidArgs {

@@ -490,11 +490,19 @@ struct ResVals {
   double p;        // pressure residual at node (kx0-2+t, sp+1), 0 outside
 };
 // ring layout of the sweep kernel (x 6 pairs, p 8 rows, b 2 pairs, b_p 2 rows)
+// b values of residual column set t (lattice columns rc0 + 2t, +1 / node kx0-2+t)
+// from the ring's b rows; a ring may instead read them from global memory
+#define SVK_RING_B_FROM_SMEM                                                                       \
+  __device__ __forceinline__ double2 b2(const double* sm, int j, int c, int t) const {            \
+    return lds2(sm + b(j, c) + 2 * t);                                                           \
+  }                                                                                              \
+  __device__ __forceinline__ double bp1(const double* sm, int r, int t) const { return sm[bp(r) + t]; }
 struct RingFz {
   static __device__ __forceinline__ int x(int j, int c) { return xrow(j, c); }
   static __device__ __forceinline__ int p(int r) { return prow(r); }
   static __device__ __forceinline__ int b(int j, int c) { return brow(j, c); }
   static __device__ __forceinline__ int bp(int r) { return bprow(r); }
+  SVK_RING_B_FROM_SMEM
 };
 // MASK = false (the fused sweep): Dirichlet / boundary-pressure rows are not
 // masked -- generic patches, the only readers of these residuals, have windows
@@ -592,14 +600,14 @@ __device__ __forceinline__ ResVals residual_from_win(const double* sm, const Lev
   ResVals R;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
-    const double2 b0 = NOB ? make_double2(0.0, 0.0) : lds2(sm + rg.b(j0, comp) + 2 * t);
-    const double2 b1 = NOB ? make_double2(0.0, 0.0) : lds2(sm + rg.b(j1, comp) + 2 * t);
+    const double2 b0 = NOB ? make_double2(0.0, 0.0) : rg.b2(sm, j0, comp, t);
+    const double2 b1 = NOB ? make_double2(0.0, 0.0) : rg.b2(sm, j1, comp, t);
     R.u[comp][0] = (!MASK || (j0ok && c0ok)) ? b0.x - ax[4 * comp + 0] : 0.0;
     R.u[comp][1] = (!MASK || (j0ok && c1ok)) ? b0.y - ax[4 * comp + 1] : 0.0;
     R.u[comp][2] = (!MASK || (j1ok && c0ok)) ? b1.x - ax[4 * comp + 2] : 0.0;
     R.u[comp][3] = (!MASK || (j1ok && c1ok)) ? b1.y - ax[4 * comp + 3] : 0.0;
   }
-  R.p = (!MASK || pok) ? (NOB ? 0.0 : sm[rg.bp(nrow) + t]) - bu : 0.0;
+  R.p = (!MASK || pok) ? (NOB ? 0.0 : rg.bp1(sm, nrow, t)) - bu : 0.0;
   return R;
 }
 
@@ -646,6 +654,7 @@ struct RingFzStep {
   __device__ __forceinline__ int p(int r) const { return prow(r); }
   __device__ __forceinline__ int b(int j, int c) const { return brow(j, c); }
   __device__ __forceinline__ int bp(int r) const { return bprow(r); }
+  SVK_RING_B_FROM_SMEM
 };
 template <bool XZERO, bool NOB = false, int RRN = fz::RR, int ORSB = fz::ORS, int ORPB = fz::ORP>
 __device__ __forceinline__ void fused_residual(double* sm, const LevelGeom& g, const FusedFactors& F, int sp,
