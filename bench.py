@@ -64,7 +64,7 @@ def measured_peaks():
 
 def measured_dfma_tflops():
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as f:
             return float(json.load(f)["fp64_fma_tflops"])
     except (OSError, ValueError, KeyError):
         return None
@@ -340,7 +340,7 @@ def run_svk(args):
     dfma = measured_dfma_tflops()
     if dfma:
         roofline["frac_of_measured_dfma"] = {"value": achieved_tf / dfma, "measured_tflops": dfma,
-                                             "source": "profiles/r1_fp64_peak.json (tools/fp64_peak.cu)"}
+                                             "source": "profiles/r2_fp64_peak.json (tools/fp64_peak.cu)"}
     roofline["paper_equivalent_tflops"] = 5202 * nodes / t_sweep / 1e12
 
     # second roofline entry: the FGMRES orthogonalisation (mat-vec + Gram-Schmidt
