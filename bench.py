@@ -426,8 +426,8 @@ def run_emulated(args):
     import torch
     from paper_2401_06277_b200 import Solver
     P, N = args.gpus, args.n
-    Ss = [Solver(N, rank=r, nranks=P, transport="emulated", agglom_rows=args.agglom, emul_group=4242)
-          for r in range(P)]
+    Ss = [Solver(N, rank=r, nranks=P, transport="emulated", agglom_rows=args.agglom, emul_group=4242,
+                 low_memory=args.low_memory) for r in range(P)]
     res, errs = [None] * P, []
 
     def body(r):
