@@ -421,14 +421,17 @@ def run_emulated(args):
     """--emulate: args.gpus logical ranks in threads on cuda:0 through the EMULATED
     transport (row slabs, halo exchanges, agglomeration all-gather, all-reduced
     dots; only the byte mover differs from NCCL).  A logic check of the
-    multi-GPU path at full size, not a multi-GPU measurement."""
+    multi-GPU path at full size, not a multi-GPU measurement.  Every rank holds
+    full-size b and x (as each GPU would), so P ranks on one GPU need P of them:
+    4096^2 with 8 ranks fits one B200, 8192^2 does not.  A failing rank ends the
+    process (the others would wait at the next emulated barrier)."""
     import threading
     import torch
     from paper_2401_06277_b200 import Solver
     P, N = args.gpus, args.n
     Ss = [Solver(N, rank=r, nranks=P, transport="emulated", agglom_rows=args.agglom, emul_group=4242,
                  low_memory=args.low_memory) for r in range(P)]
-    res, errs = [None] * P, []
+    res = [None] * P
 
     def body(r):
         try:
@@ -451,16 +454,16 @@ def run_emulated(args):
                 e1.record(st)
                 st.synchronize()
                 res[r] = (e0.elapsed_time(e1) / 1e3, its, rep["rel_residual"], S.device_bytes)
-        except BaseException as e:  # noqa: BLE001
-            errs.append(e)
+        except BaseException as e:  # noqa: BLE001 - the other ranks would wait at the next emulated barrier
+            sys.stderr.write("emulated rank %d failed: %r\n" % (r, e))
+            sys.stderr.flush()
+            os._exit(1)
 
     th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
     for t in th:
         t.start()
     for t in th:
         t.join()
-    if errs:
-        raise errs[0]
     t = max(q[0] for q in res)
     line = {"metric": METRIC, "value": n_dof(N) * args.steps / t, "unit": "DOF/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
