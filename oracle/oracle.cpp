@@ -26,12 +26,16 @@
 // lattice point (i,j) sits at (i*h/2, j*h/2); pressure node (kx,ky) at (kx*h, ky*h).
 // Level 0 is the coarsest (alg:mg); level L-1 the finest.
 //
-// parity pins (tests/test_oracle_*.py): brute-force dense NumPy checker for
-// N<=8, nodal exactness of two manufactured solutions, symmetry / null vector,
-// 25 patch groups and tab:rwf counts, Galerkin identity, pinv for the coarse
-// solve, FGMRES against its least-squares definition.  The V-cycle's
-// convergence factor is "parity unpinned" against the paper (the paper prints
-// none) -- it is pinned only by the internal checks above.
+// parity pins (tests/test_oracle*.py): brute-force dense NumPy checker for
+// N<=16 (operator, sweep, V-cycle incl. the three-sweep level-0 mode, scalar
+// weighting, BS / SU with finite Jacobi sweeps, block-triangular with finite
+// cycles), nodal exactness of two manufactured solutions, the closed-form
+// cavity data and the cavity solution's mirror symmetry, symmetry / null
+// vector, 25 patch groups and tab:rwf counts, Galerkin identity, pinv for the
+// coarse solve, FGMRES against its least-squares definition, and the local
+// full-size samplers against the global oracle.  Every function is pinned; the
+// paper prints no V-cycle convergence factors or iteration counts, so those two
+// PROPERTIES have no paper value to compare with.
 // =============================================================================
 #include <algorithm>
 #include <cmath>
