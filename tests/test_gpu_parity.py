@@ -327,3 +327,23 @@ def test_low_memory_krylov_matches_fgmres(gpu, N, kind):
     assert np.abs(x1g[:2 * nv] - xo[:2 * nv]).max() < 1e-8 * scale
     assert np.abs(x1g[:2 * nv] - x0g[:2 * nv]).max() < 1e-9 * scale
     assert m1 < m0
+
+
+def test_degenerate_cases_single_level_and_zero_rhs(gpu):
+    """As the oracle pin: N = N0 (one level: the V-cycle is the exact min-norm solve)
+    converges in one FGMRES iteration to the oracle's solution; b = 0, x0 = 0 needs
+    none and returns x = 0."""
+    from paper_2401_06277_b200 import Solver
+    S, O = Solver(4, n_coarse=4), oracle.Oracle(4, n_coarse=4)
+    b, x = S.set_problem("mms_paper")
+    rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=10)
+    bo, x0o = O.problem(oracle.MMS_PAPER)
+    xo, its, _, _, _ = O.fgmres(bo, x0o, rtol=1e-10, maxit=10)
+    assert rep["converged"] == 1 and rep["iterations"] == its == 1
+    xg = to_np(S, x, S.fine)
+    nv = 9 * 9
+    assert np.abs(xg[:2 * nv] - xo[:2 * nv]).max() < 1e-12
+    z = S.new_vector()
+    xz = S.new_vector()
+    rep, hist = S.fgmres(z, xz, rtol=1e-10, maxit=10)
+    assert rep["converged"] == 1 and rep["iterations"] == 0 and float(xz.abs().max()) == 0.0

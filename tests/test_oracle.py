@@ -377,3 +377,17 @@ def test_sampled_transfers_equal_global_oracle(N):
     xf = svk_inputs.random_vector(N, 34)
     idxf = np.arange(o.length(l), dtype=np.int64)
     assert rel(oracle.prolong_sample(N, ec, xf, idxf) - xf, o.prolong_add(l, ec, xf) - xf) < 1e-14
+
+
+def test_degenerate_cases_single_level_and_zero_rhs():
+    """Degenerate cases of the method: with a single level (N = N0) the V-cycle is
+    the exact minimum-norm solve, so FGMRES with that exact preconditioner
+    converges in one iteration; a zero right-hand side with zero initial guess
+    needs none."""
+    o = oracle.Oracle(4, n_coarse=4)
+    b, x0 = o.problem(oracle.MMS_PAPER)
+    x, its, hist, tr, st = o.fgmres(b, x0, rtol=1e-10, maxit=10)
+    assert st == 0 and its == 1 and tr < 1e-12
+    z = np.zeros_like(b)
+    x, its, hist, tr, st = o.fgmres(z, z, rtol=1e-10, maxit=10)
+    assert st == 0 and its == 0 and np.all(x == 0)
