@@ -171,7 +171,8 @@ def prolongation(Nc: int) -> np.ndarray:
 class DenseMG:
     """Dense V(1,1) per alg:mg on brute-force components."""
 
-    def __init__(self, N: int, N0: int = 4, nu: float = 1.0, omega: float = 0.8):
+    def __init__(self, N: int, N0: int = 4, nu: float = 1.0, omega: float = 0.8, nu1: int = 1, nu2: int = 1):
+        self.nu1, self.nu2 = nu1, nu2
         self.levels = []
         n = N0
         while n <= N:
@@ -190,13 +191,16 @@ class DenseMG:
         if l == 0:
             return self.coarse(b)
         Lv = self.levels[l]
-        x = Lv.sweep(x, b)
+        for _ in range(self.nu1):
+            x = Lv.sweep(x, b)
         r = Lv.residual(x, b)
         rc = self.P[l].T @ r
         rc[self.levels[l - 1].dir] = 0.0
         ec = self.coarse(rc) if l == 1 else self.mg(l - 1, rc, np.zeros_like(rc))
         x = x + self.P[l] @ ec
-        return Lv.sweep(x, b)
+        for _ in range(self.nu2):
+            x = Lv.sweep(x, b)
+        return x
 
     def vcycle(self, b, x=None):
         x = np.zeros_like(b) if x is None else x

@@ -391,3 +391,34 @@ def test_degenerate_cases_single_level_and_zero_rhs():
     z = np.zeros_like(b)
     x, its, hist, tr, st = o.fgmres(z, z, rtol=1e-10, maxit=10)
     assert st == 0 and its == 0 and np.all(x == 0)
+
+
+@pytest.mark.parametrize("nu", [0.37, 7.5])
+def test_viscosity_operator_and_sweep_vs_bruteforce(nu):
+    """nu != 1: L = nu (M (x) K + K (x) M) while B is unchanged -- the assembled
+    operator and one Vanka sweep against the brute force built with the same nu."""
+    N = 8
+    o = oracle.Oracle(N, n_coarse=N, nu=nu)
+    B = brute.full_operator(N, nu)
+    A = o.csr(0).toarray()
+    assert np.abs(A - B).max() <= 1e-14 * np.abs(B).max()
+    D = brute.Dense(N, nu=nu)
+    x = svk_inputs.random_vector(N, 71)
+    b = svk_inputs.random_vector(N, 72)
+    assert rel(o.sweep(0, x, b) - x, D.sweep(x, b) - x) < 1e-12
+    # sensitivity: the nu = 1 operator differs
+    assert np.abs(brute.full_operator(N, 1.0) - B).max() > 1e-3 * np.abs(B).max()
+
+
+@pytest.mark.parametrize("nu1,nu2,omega", [(2, 2, 0.7), (0, 1, 0.8), (1, 0, 0.8), (3, 1, 0.6)])
+def test_vcycle_smoothing_counts_vs_dense_mg(nu1, nu2, omega):
+    """V(nu1, nu2) (alg:mg) with other sweep counts and weights against
+    the dense brute-force multigrid with the same counts; another count differs."""
+    N = 16
+    o = oracle.Oracle(N, omega=omega, nu1=nu1, nu2=nu2)
+    M = brute.DenseMG(N, omega=omega, nu1=nu1, nu2=nu2)
+    b = svk_inputs.random_vector(N, 81)
+    b[o.dirichlet(o.fine)] = 0
+    want = M.vcycle(b)
+    assert rel(o.vcycle(b), want) < 1e-12
+    assert rel(brute.DenseMG(N, omega=omega, nu1=nu1 + 1, nu2=nu2).vcycle(b), want) > 1e-6
