@@ -222,6 +222,8 @@ class Transport {
   virtual int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) = 0;
   // whether its operations may be captured into a CUDA graph (stream-ordered, no host sync)
   virtual bool capturable() const = 0;
+  // an asynchronous communication error since the last call (NCCL: ncclCommGetAsyncError), 0 if none
+  virtual int async_error(std::string& err) { (void)err; return 0; }
 };
 
 // ----------------------------------------------------------------- NCCL
@@ -241,6 +243,7 @@ struct NcclApi {
   ncclResult_t_ (*AllGather)(const void*, void*, size_t, int, ncclComm_t_, cudaStream_t) = nullptr;
   ncclResult_t_ (*GroupStart)() = nullptr;
   ncclResult_t_ (*GroupEnd)() = nullptr;
+  ncclResult_t_ (*CommGetAsyncError)(ncclComm_t_, ncclResult_t_*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t_) = nullptr;
   bool ok() const {
     return h && GetUniqueId && CommInitRank && Send && Recv && AllReduce && AllGather && GroupStart && GroupEnd;
@@ -266,6 +269,7 @@ inline NcclApi& nccl_api() {
     api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(api.h, "ncclCommGetAsyncError");
   });
   return api;
 }
@@ -319,6 +323,16 @@ class NcclTransport : public Transport {
     return 0;
   }
   bool capturable() const override { return true; }  // NCCL operations are stream-capturable
+  int async_error(std::string& err) override {
+    NcclApi& a = nccl_api();
+    if (!a.CommGetAsyncError || !comm_) return 0;
+    ncclResult_t_ r = 0;
+    if (a.CommGetAsyncError(comm_, &r) != 0 || r != 0) {
+      err = std::string("NCCL asynchronous error: ") + (a.GetErrorString ? a.GetErrorString(r) : "error");
+      return -1;
+    }
+    return 0;
+  }
   int allgather(const double* send, double* recv, int64_t count, cudaStream_t s, std::string& err) override {
     if (nccl_api().AllGather(send, recv, (size_t)count, kNcclDouble, comm_, s) != 0) {
       err = "ncclAllGather failed";
@@ -388,14 +402,23 @@ class EmulTransport : public Transport {
     G.hi_send[rank_] = hi_send;
     G.barrier();
     // my lo_recv = (rank-1)'s hi_send; my hi_recv = (rank+1)'s lo_send
-    for (size_t k = 0; k < lo_recv.size(); ++k)
-      cudaMemcpy(lo_recv[k].ptr, G.hi_send[rank_ - 1][k].ptr, lo_recv[k].count * sizeof(double),
-                 cudaMemcpyDeviceToDevice);
-    for (size_t k = 0; k < hi_recv.size(); ++k)
-      cudaMemcpy(hi_recv[k].ptr, G.lo_send[rank_ + 1][k].ptr, hi_recv[k].count * sizeof(double),
-                 cudaMemcpyDeviceToDevice);
-    G.barrier();
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    cudaError_t e = cudaSuccess;
+    for (size_t k = 0; k < lo_recv.size(); ++k) {
+      const cudaError_t ek = cudaMemcpy(lo_recv[k].ptr, G.hi_send[rank_ - 1][k].ptr, lo_recv[k].count * sizeof(double),
+                                        cudaMemcpyDeviceToDevice);
+      if (e == cudaSuccess) e = ek;
+    }
+    for (size_t k = 0; k < hi_recv.size(); ++k) {
+      const cudaError_t ek = cudaMemcpy(hi_recv[k].ptr, G.lo_send[rank_ + 1][k].ptr, hi_recv[k].count * sizeof(double),
+                                        cudaMemcpyDeviceToDevice);
+      if (e == cudaSuccess) e = ek;
+    }
+    G.barrier();  // every rank reaches it, also on error (no rank may be left waiting)
+    if (e != cudaSuccess) {
+      err = std::string("emulated exchange: copy failed: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return 0;
   }
   int allreduce_sum(double* buf, int64_t count, cudaStream_t s, std::string& err) override {
     EmulGroup& G = *group_;
@@ -410,7 +433,11 @@ class EmulTransport : public Transport {
     for (int r = 0; r < G.nranks; ++r)  // fixed rank order: deterministic
       for (int64_t i = 0; i < count; ++i) sum[i] += G.red[r][i];
     G.barrier();
-    cudaMemcpy(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice);
+    if (const cudaError_t e = cudaMemcpy(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice);
+        e != cudaSuccess) {
+      err = std::string("emulated allreduce: copy back failed: ") + cudaGetErrorString(e);
+      return -1;
+    }
     return 0;
   }
   bool capturable() const override { return false; }  // host barriers
@@ -421,13 +448,20 @@ class EmulTransport : public Transport {
     }
     EmulGroup& G = *group_;
     std::vector<double> mine((size_t)count);  // a copy, so that send may alias recv
-    cudaMemcpy(mine.data(), send, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(mine.data(), send, count * sizeof(double), cudaMemcpyDeviceToHost);
     G.red[rank_] = mine;
     G.barrier();
-    for (int r = 0; r < G.nranks; ++r)
-      cudaMemcpy(recv + (int64_t)r * count, G.red[r].data(), count * sizeof(double), cudaMemcpyHostToDevice);
+    for (int r = 0; r < G.nranks; ++r) {
+      const cudaError_t er = cudaMemcpy(recv + (int64_t)r * count, G.red[r].data(), count * sizeof(double),
+                                        cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = er;
+    }
     G.barrier();
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    if (e != cudaSuccess) {
+      err = std::string("emulated allgather: copy failed: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return 0;
   }
 
  private:

@@ -1091,6 +1091,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       TRY(harvest_graph_prof(ctx));
+      if (ctx->tr && ctx->tr->async_error(ctx->err) != 0) return SVK_ERR_NCCL;  // polled once per iteration
       float a01 = 0, a12 = 0;
       cudaEventElapsedTime(&a01, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&a12, ctx->ev[1], ctx->ev[2]);
