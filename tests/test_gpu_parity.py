@@ -347,3 +347,18 @@ def test_degenerate_cases_single_level_and_zero_rhs(gpu):
     xz = S.new_vector()
     rep, hist = S.fgmres(z, xz, rtol=1e-10, maxit=10)
     assert rep["converged"] == 1 and rep["iterations"] == 0 and float(xz.abs().max()) == 0.0
+
+
+def test_not_converged_is_reported_and_matches_oracle_history(gpu):
+    """maxit below the needed count: SVK_NOT_CONVERGED (status 1, non-fatal), the
+    report filled, and the truncated residual history equal to the oracle's."""
+    N = 64
+    S, O = get_solver(N), get_oracle(N)
+    b, x = S.set_problem("mms_paper")
+    rep, hist = S.fgmres(b, x, rtol=1e-10, maxit=5)
+    assert rep["status"] == 1 and rep["converged"] == 0 and rep["iterations"] == 5 and len(hist) == 6
+    bo, x0o = O.problem(oracle.MMS_PAPER)
+    xo, its, ho, tro, st = O.fgmres(bo, x0o, rtol=1e-10, maxit=5)
+    assert st == 1 and its == 5
+    assert np.all(np.abs(hist - ho) <= 1e-9 * ho)
+    assert abs(rep["rel_residual"] - tro) <= 1e-8 * tro
