@@ -400,7 +400,7 @@ def run_svk(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper manufactured solution, P:76-81)",
             "config": config_dict(args, world),
             "time_to_solve_s": ms_step / 1e3, "iterations": its[-1], "iterations_all": its, "step_ms": step_ms,
-            "rel_residual": reps[-1]["rel_residual"], "setup_s": setup_s,
+            "rel_residual": reps[-1]["rel_residual"], "setup_s": setup_s, "t_setup_s": reps[-1]["t_setup_s"],
             "t_vcycle_s": reps[-1]["t_vcycle_s"], "t_orth_s": reps[-1]["t_orth_s"],
             "sweep": {"dof_per_s": n_dof(N) * share / t_sweep, "slab_share": share, "ms": 1e3 * t_sweep, "hbm_gbs_alg": sweep_gbs,
                       "hbm_frac": sweep_gbs / hbm_peak, "gflops_alg": achieved_tf * 1e3},

@@ -165,6 +165,25 @@ typedef struct svk_config {
                              preconditioned GMRES), half the Krylov memory (8192^2 fits
                              one B200).  Not with BLOCK_TRIANGULAR (kept as FGMRES). */
   int32_t reserved0;
+  /* Optional device allocator for the context's vector-sized workspaces (level
+   * work vectors, the Krylov basis, boundary-patch staging, host-solve staging),
+   * e.g. to route them through a framework's caching allocator (the Python
+   * binding's Solver(allocator="torch") passes torch.cuda.caching_allocator_*).
+   * Both or neither must be set (else svk_create returns SVK_ERR_INVALID).
+   * alloc_fn(bytes, device, user) returns device memory on cfg.device aligned to
+   * 256 bytes, or NULL (the calling entry point then returns SVK_ERR_CUDA); the
+   * library zero-fills it after a device synchronisation, so the memory may have
+   * been in use on any stream before.  free_fn(ptr, bytes, device, user) is called
+   * once per block, from svk_destroy after a device synchronisation (no kernel of
+   * the context uses the block any more).  Calls happen inside svk_create and, for
+   * lazily sized workspaces, inside the first svk_fgmres / svk_solve_host /
+   * svk_vcycle of a size -- from the thread making that call.  Small tables
+   * (patch factors, coefficients, the coarse LU) and the slab-local vectors of
+   * distributed levels (mapped with the CUDA VMM API) always use the driver.
+   * NULL (default): cudaMalloc / cudaFree. */
+  void* (*alloc_fn)(int64_t bytes, int32_t device, void* user);
+  void (*free_fn)(void* ptr, int64_t bytes, int32_t device, void* user);
+  void* alloc_user;
 } svk_config;
 
 /* FGMRES preconditioner:
@@ -224,6 +243,8 @@ typedef struct svk_report {
   double t_total_s;        /* wall time of the call (host clock) */
   double t_vcycle_s;       /* device time in V-cycles (CUDA events) */
   double t_orth_s;         /* device time in matvec + orthogonalisation */
+  double t_setup_s;        /* wall time (host clock) svk_create spent building this
+                              context: hierarchy, patch factors, coarse LU, validation */
 } svk_report;
 
 typedef struct svk_ctx svk_ctx;

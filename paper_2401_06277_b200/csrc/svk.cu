@@ -102,6 +102,7 @@ struct svk_ctx {
   // multi-GPU row slabs (dist.cuh): levels la..nlev-1 are distributed
   std::unique_ptr<Transport> tr;
   int la = 1 << 30;
+  double t_setup_s = 0.0;  // svk_create wall time (svk_report.t_setup_s)
   bool poison = false;  // SVK_POISON_HALO=1: NaN-fill rows beyond the halo after each exchange (tests)
   std::string err;
 };
@@ -274,8 +275,22 @@ int valid_ptr(svk_ctx* ctx, const void* p, const char* what) {
 }
 
 int alloc_vec(svk_ctx* ctx, double** p, int64_t n) {
-  CK(cudaMalloc(p, n * sizeof(double)));
-  CK(cudaMemset(*p, 0, n * sizeof(double)));
+  const int64_t bytes = n * (int64_t)sizeof(double);
+  if (ctx->cfg.alloc_fn) {
+    // caller's allocator (svk_config.alloc_fn): the block may have been in use on
+    // any stream until now, so order the zero-fill after all of the device's work
+    CK(cudaDeviceSynchronize());
+    *p = (double*)ctx->cfg.alloc_fn(bytes, ctx->cfg.device, ctx->cfg.alloc_user);
+    if (!*p || ((uintptr_t)*p & 255u)) {
+      if (*p) ctx->cfg.free_fn(*p, bytes, ctx->cfg.device, ctx->cfg.alloc_user);
+      *p = nullptr;
+      ctx->err = "svk_config.alloc_fn returned NULL or a block not aligned to 256 bytes";
+      return SVK_ERR_CUDA;
+    }
+  } else {
+    CK(cudaMalloc(p, bytes));
+  }
+  CK(cudaMemset(*p, 0, bytes));
   ctx->dev_bytes += n * (int64_t)sizeof(double);
   ctx->plain_bytes[*p] = n * (int64_t)sizeof(double);
   return SVK_OK;
@@ -292,8 +307,13 @@ void free_vec(svk_ctx* ctx, double* p) {
   }
   auto jt = ctx->plain_bytes.find(p);
   if (jt != ctx->plain_bytes.end()) {
-    ctx->dev_bytes -= jt->second;
+    const int64_t bytes = jt->second;
+    ctx->dev_bytes -= bytes;
     ctx->plain_bytes.erase(jt);
+    if (ctx->cfg.free_fn) {
+      ctx->cfg.free_fn(p, bytes, ctx->cfg.device, ctx->cfg.alloc_user);
+      return;
+    }
   }
   cudaFree(p);
 }
@@ -1194,6 +1214,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   R.t_vcycle_s = tv;
   R.t_orth_s = to;
   R.t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  R.t_setup_s = ctx->t_setup_s;
   if (status == SVK_OK && !conv) status = SVK_NOT_CONVERGED;
   if (status == SVK_OK && !std::isfinite(R.rel_residual)) status = SVK_ERR_NONFINITE;
   R.status = status;
@@ -1202,8 +1223,12 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
 }
 
 int free_ctx(svk_ctx* ctx) {
-  auto F = [](void* p) {
-    if (p) cudaFree(p);
+  auto F = [ctx](void* p) {  // alloc_vec blocks go back to their allocator
+    if (!p) return;
+    if (ctx->plain_bytes.count((const double*)p))
+      free_vec(ctx, (double*)p);
+    else
+      cudaFree(p);
   };
   F(ctx->d_Ns);
   F(ctx->d_inv);
@@ -1549,9 +1574,12 @@ int svk_create(const svk_config* cfg, svk_ctx** out) {
   if (cfg->nranks > 1 && (cfg->agglom_rows < kHalo || cfg->sweep_impl != SVK_SWEEP_FUSED ||
                           (cfg->transport != SVK_TRANSPORT_NCCL && cfg->transport != SVK_TRANSPORT_EMULATED)))
     return SVK_ERR_INVALID;
+  if ((cfg->alloc_fn == nullptr) != (cfg->free_fn == nullptr)) return SVK_ERR_INVALID;
+  const auto t0 = std::chrono::steady_clock::now();
   svk_ctx* ctx = new svk_ctx;
   ctx->cfg = *cfg;
   int st = guarded(ctx, [&]() -> int { return create_impl(ctx); });
+  ctx->t_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (st != SVK_OK) {
     std::fprintf(stderr, "svk_create: %s\n", ctx->err.c_str());
     free_ctx(ctx);

@@ -42,7 +42,30 @@ class Config(C.Structure):
                 ("relax_t", C.c_double), ("relax_omega", C.c_double), ("jacobi_omega", C.c_double),
                 ("precond", C.c_int32), ("bt_cycles", C.c_int32), ("bt_nu", C.c_int32), ("validate", C.c_int32),
                 ("bt_omega_u", C.c_double), ("bt_omega_p", C.c_double), ("krylov_store_z", C.c_int32),
-                ("reserved0", C.c_int32)]
+                ("reserved0", C.c_int32), ("alloc_fn", C.c_void_p), ("free_fn", C.c_void_p),
+                ("alloc_user", C.c_void_p)]
+
+# svk_config.alloc_fn / free_fn
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
+def torch_allocator_callbacks():
+    """(alloc_fn, free_fn) routing svk workspaces through torch's CUDA caching
+    allocator (torch.cuda.caching_allocator_alloc / _delete, on the device's
+    current stream); keep the returned objects alive as long as the context."""
+    import torch
+
+    def _alloc(nbytes, device, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device)
+        except Exception:   # NULL -> SVK_ERR_CUDA from the calling entry point
+            return None
+
+    def _free(ptr, nbytes, device, user):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 class LevelInfo(C.Structure):
@@ -55,7 +78,7 @@ class LevelInfo(C.Structure):
 class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("n_reorth", C.c_int32),
                 ("rel_residual", C.c_double), ("t_total_s", C.c_double), ("t_vcycle_s", C.c_double),
-                ("t_orth_s", C.c_double)]
+                ("t_orth_s", C.c_double), ("t_setup_s", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -159,12 +182,14 @@ class Solver:
                  relax_omega: float | None = None, jacobi_omega: float | None = None,
                  jacobi_sweeps: int | None = None, precond: str = "mg", bt_cycles: int = 3, bt_nu: int = 3,
                  bt_omega_u: float = 1.0, bt_omega_p: float = 0.6, validate: bool = False,
-                 low_memory: bool = False):
+                 low_memory: bool = False, allocator: str = "cuda"):
         """nranks > 1: row-slab multi-GPU mode (include/svk.h, MULTI-GPU).  transport "nccl" needs
         `nccl_id` (128 bytes from `nccl_unique_id()` on rank 0, see `nccl_id_broadcast`);
         "emulated" runs nranks logical ranks of one process on one device (one thread each).
         relax: "vanka" (the hot path), "bs" (Braess-Sarazin) or "su" (Schur-Uzawa) comparators;
-        unset comparator parameters take RELAX_DEFAULTS[relax]."""
+        unset comparator parameters take RELAX_DEFAULTS[relax].
+        allocator: "cuda" (cudaMalloc) or "torch" (vector workspaces from torch's
+        caching allocator, svk_config.alloc_fn)."""
         import torch
         if not torch.cuda.is_available():
             raise SvkError("libsvk needs a CUDA device (B200, sm_100a); none is visible")
@@ -192,6 +217,13 @@ class Solver:
             if len(nccl_id) != 128:
                 raise SvkError("nccl_id must be 128 bytes")
             C.memmove(cfg.nccl_id, bytes(nccl_id), 128)
+        self._alloc_cbs = None
+        if allocator == "torch":
+            self._alloc_cbs = torch_allocator_callbacks()
+            cfg.alloc_fn = C.cast(self._alloc_cbs[0], C.c_void_p)
+            cfg.free_fn = C.cast(self._alloc_cbs[1], C.c_void_p)
+        elif allocator != "cuda":
+            raise SvkError("allocator must be 'cuda' or 'torch'")
         self.rank, self.nranks = rank, nranks
         self.cfg = cfg
         self.device = torch.device("cuda", device)

@@ -60,3 +60,39 @@ def test_config_defaults_and_invalid_configs(lib_path):
         c.n_coarse = bad["n_coarse"]
         assert lib.svk_create(C.byref(c), C.byref(h)) == -1   # rejected before touching the GPU
     assert lib.svk_destroy(None) == -1
+
+
+@pytest.mark.parametrize("cname,pyname", [("svk_config", "Config"), ("svk_level", "LevelInfo"),
+                                          ("svk_report", "Report")])
+def test_struct_layouts_match_header(cname, pyname, tmp_path):
+    """The ctypes structures of the binding have the header's field offsets and size
+    (a C program built against include/svk.h prints offsetof of every field)."""
+    import ctypes as C
+    from paper_2401_06277_b200 import svk
+    py = getattr(svk, pyname)
+    fields = [f for f, _ in py._fields_]
+    prog = tmp_path / "layout.c"
+    prog.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"svk.h\"\nint main(void) {\n"
+                    + "".join('  printf("%%s %%zu\\n", "%s", offsetof(%s, %s));\n' % (f, cname, f) for f in fields)
+                    + '  printf("sizeof %%zu\\n", sizeof(%s));\n  return 0;\n}\n' % cname)
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for f in fields:
+        assert int(out[f]) == getattr(py, f).offset, f
+    assert int(out["sizeof"]) == C.sizeof(py)
+
+
+def test_allocator_callbacks_both_or_neither(lib_path):
+    import ctypes as C
+    from paper_2401_06277_b200 import svk
+    lib = svk.load_library(lib_path)
+    alloc, free = svk.ALLOC_FN(lambda n, d, u: None), svk.FREE_FN(lambda p, n, d, u: None)
+    h = C.c_void_p()
+    for a, f in ((alloc, None), (None, free)):
+        c = svk.Config()
+        lib.svk_config_default(C.byref(c), 64)
+        c.alloc_fn = C.cast(a, C.c_void_p) if a else None
+        c.free_fn = C.cast(f, C.c_void_p) if f else None
+        assert lib.svk_create(C.byref(c), C.byref(h)) == -1   # rejected before touching the GPU
