@@ -96,6 +96,53 @@ __device__ __forceinline__ double div_at(const double* __restrict__ ux, const do
   return -h * s;
 }
 
+// The same three stencils with the vector read through an accessor u(i, j) /
+// p(kx, ky) / u(comp, i, j) (same loops and summation order as lap_at / gradp_at /
+// div_at): the boundary-patch kernel evaluates them on a band staged in shared memory.
+template <class U>
+__device__ __forceinline__ double lap_f(const U& u, int i, int j) {
+  const int pi = i & 1, pj = j & 1;
+  const int ra = pi ? 1 : 2, rb = pj ? 1 : 2;
+  double s = 0.0;
+  for (int bb = -rb; bb <= rb; ++bb) {
+    const double my = c_st.MR[pj][bb + 2], ky = c_st.KR[pj][bb + 2];
+    for (int aa = -ra; aa <= ra; ++aa) s += (my * c_st.KR[pi][aa + 2] + ky * c_st.MR[pi][aa + 2]) * u(i + aa, j + bb);
+  }
+  return s;
+}
+template <class P>
+__device__ __forceinline__ double gradp_f(const P& p, int i, int j, int comp, double h) {
+  const int pi = i & 1, pj = j & 1;
+  const int ky0 = pj ? (j - 1) >> 1 : (j >> 1) - 1, nky = pj ? 2 : 3;
+  const int kx0 = pi ? (i - 1) >> 1 : (i >> 1) - 1, nkx = pi ? 2 : 3;
+  double s = 0.0;
+  for (int ty = 0; ty < nky; ++ty) {
+    const double cy = comp == 0 ? c_st.CC[pj][ty] : c_st.GC[pj][ty];
+    if (cy == 0.0) continue;
+    double t = 0.0;
+    for (int tx = 0; tx < nkx; ++tx) t += (comp == 0 ? c_st.GC[pi][tx] : c_st.CC[pi][tx]) * p(kx0 + tx, ky0 + ty);
+    s += cy * t;
+  }
+  return -h * s;
+}
+template <class U>
+__device__ __forceinline__ double div_f(const U& u, int N, int kx, int ky, double h) {
+  const int cx = kx == 0 ? 0 : (kx == N ? 2 : 1), cy = ky == 0 ? 0 : (ky == N ? 2 : 1);
+  const int lat = 2 * N + 1;
+  double s = 0.0;
+  for (int oy = 0; oy < 5; ++oy) {
+    const int j = 2 * ky - 2 + oy;
+    if (j < 0 || j >= lat) continue;
+    const double cyc = c_st.CR[cy][oy], gyc = c_st.GR[cy][oy];
+    for (int ox = 0; ox < 5; ++ox) {
+      const int i = 2 * kx - 2 + ox;
+      if (i < 0 || i >= lat) continue;
+      s += cyc * c_st.GR[cx][ox] * u(0, i, j) + gyc * c_st.CR[cx][ox] * u(1, i, j);
+    }
+  }
+  return -h * s;
+}
+
 // r = b - A x (WITH_B) or r = A x, masked to 0 on Dirichlet rows; padding -> 0.
 // grid: x over columns (pitch), y over rows, z = plane (0 ux, 1 uy, 2 p)
 template <bool WITH_B>

@@ -103,6 +103,8 @@ struct svk_ctx {
   std::unique_ptr<Transport> tr;
   int la = 1 << 30;
   double t_setup_s = 0.0;  // svk_create wall time (svk_report.t_setup_s)
+  cudaEvent_t sweep_ev0 = nullptr;  // start event of the next timed sweep (op_sweep -> op_sweep_impl)
+  unsigned sweep_ev0_flags = 0;
   bool poison = false;  // SVK_POISON_HALO=1: NaN-fill rows beyond the halo after each exchange (tests)
   std::string err;
 };
@@ -509,7 +511,8 @@ int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
     ctx->capturing->ev.emplace_back(e0, e1);
     // cudaEventRecordExternal: real event-record nodes in the captured graph
     // (a plain record during capture only expresses a dependency)
-    CK(cudaEventRecordWithFlags(e0, s, cudaEventRecordExternal));
+    ctx->sweep_ev0 = e0;
+    ctx->sweep_ev0_flags = cudaEventRecordExternal;
     TRY(op_sweep_impl(ctx, l, xin, b, xout, x_zero, s));
     CK(cudaEventRecordWithFlags(e1, s, cudaEventRecordExternal));
     return SVK_OK;
@@ -520,7 +523,8 @@ int op_sweep(svk_ctx* ctx, int l, const double* xin, const double* b, double* xo
       CK(cudaEventCreate(&e));
       ctx->prof_ev.push_back(e);
     }
-    CK(cudaEventRecord(ctx->prof_ev[ctx->prof_used], s));
+    ctx->sweep_ev0 = ctx->prof_ev[ctx->prof_used];
+    ctx->sweep_ev0_flags = cudaEventRecordDefault;
   }
   TRY(op_sweep_impl(ctx, l, xin, b, xout, x_zero, s));
   if (timed) {
@@ -558,12 +562,18 @@ int op_sweep_impl(svk_ctx* ctx, int l, const double* xin, const double* b, doubl
   if (!x_zero) debug_slab_rows(ctx, l, xin, "sweep x");
   const LevelGeom& g = ctx->g[l];
   const int scalar_w = ctx->cfg.weighting == SVK_WEIGHT_SCALAR;
+  // timed sweep (op_sweep): the start event brackets the sweep kernel alone --
+  // recorded after the boundary-patch kernel in the fused path
+  const cudaEvent_t ev0 = ctx->sweep_ev0;
+  ctx->sweep_ev0 = nullptr;
+  if (ev0 && ctx->cfg.sweep_impl != SVK_SWEEP_FUSED) CK(cudaEventRecordWithFlags(ev0, s, ctx->sweep_ev0_flags));
   if (ctx->cfg.sweep_impl == SVK_SWEEP_FUSED) {
     const int lst = launch_fused_sweep(g, ctx->cfg.nu, ctx->cfg.omega_v, scalar_w, ctx->h_fac[l],
                                        ctx->d_inv + (size_t)l * 25 * kGroupStride, ctx->d_tiles[l], ctx->ntiles[l],
-                                       ctx->d_bd, x_zero ? nullptr : xin, b, xout, ctx->nsm, s);
+                                       ctx->d_bd, x_zero ? nullptr : xin, b, xout, ctx->nsm, s, ev0,
+                                       ctx->sweep_ev0_flags);
     if (lst != 0) {
-      ctx->err = "sweep: " + tma_error();
+      ctx->err = lst == -3 ? std::string("sweep: profiling event record failed") : "sweep: " + tma_error();
       return SVK_ERR_CUDA;
     }
     CKL();

@@ -251,7 +251,13 @@ __host__ __device__ __forceinline__ int64_t bd_index(int kx, int ky, int N) {
 struct BdTile {
   int kx, ky, dx, dy, n, grp;
 };
-constexpr int kBdTile = 16, kBdThreads = 512;
+#ifndef SVK_BD_TILE
+#define SVK_BD_TILE 16
+#endif
+#ifndef SVK_BD_MINB
+#define SVK_BD_MINB 1
+#endif
+constexpr int kBdTile = SVK_BD_TILE, kBdThreads = 512;
 inline std::vector<BdTile> make_bd_tiles(int N) {
   std::vector<BdTile> t;
   auto seg = [&](int kx, int ky, int dx, int dy, int n) {
@@ -275,16 +281,24 @@ inline std::vector<BdTile> make_bd_tiles(int N) {
 // (phase 1), gathered into per-patch windows (phase 2), then the dense group
 // inverse is applied (phase 3).  Dirichlet / outside points carry 0 (they are
 // excluded from the patch unknowns, P:469 reading 7).
+// x != 0: the band plus its 2-point stencil halo of x (9 x (2n+7) lattice points
+// per component, 5 x (n+4) pressure nodes) is first staged in shared memory, so
+// that each x value is read from memory once instead of by every stencil that
+// touches it (the residual then uses lap_f / gradp_f / div_f on the stage, the
+// same arithmetic as lap_at / gradp_at / div_at).
 constexpr int kBdBandW = 2 * kBdTile + 3;  // band length along the tile
-__global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
+constexpr int kBdStA = kBdBandW + 4;       // staged length along (stencil halo 2 + 2)
+__global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
                                                          const BdTile* __restrict__ tiles,
                                                          const double* __restrict__ x, const double* __restrict__ b,
                                                          double* __restrict__ bd) {
   constexpr int T = kBdTile, RS = 53;  // odd row stride: conflict-free 64-bit smem accesses
   constexpr int NBAND = 2 * 5 * kBdBandW;
+  constexpr int NXS = 2 * 9 * kBdStA, NPS = 5 * (T + 4);
   __shared__ double Ai[kGroupStride];
   __shared__ double rv[T * RS];
   __shared__ double band[NBAND + T];  // [comp][5 across][kBdBandW along] + pressure residuals
+  __shared__ double xs[NXS + NPS];    // x != 0: [comp][9 across][kBdStA along] + [5 across][T + 4 along]
   pdl_wait();
   const int N = g.N, lat = g.lat;
   const int64_t nb = bd_count(N);
@@ -296,6 +310,35 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
   // band origin: lattice point (2 kx - 2, 2 ky - 2) of the tile's first patch; "along" = tile direction
   const int i0 = 2 * tl.kx - 2, j0 = 2 * tl.ky - 2;
   const int nalong = 2 * tl.n + 3;
+  // stage: lattice (i, j) <-> [across][along] from (i0 - 2, j0 - 2); nodes from (kx - 2, ky - 2).
+  // Rows a slab-local vector does not hold are never read by the band's stencils
+  // (the stencils of band rows outside the slab's patch rows are skipped below).
+  const int jlo = 2 * (g.r0 - 1) - 4, jhi = 2 * g.r1 + 4;
+  if (x) {
+    for (int q = threadIdx.x; q < NXS + NPS; q += blockDim.x) {
+      double v = 0.0;
+      if (q < NXS) {
+        const int comp = q / (9 * kBdStA), rem = q % (9 * kBdStA), ac = rem / kBdStA, al = rem % kBdStA;
+        const int i = i0 - 2 + (tl.dx ? al : ac), j = j0 - 2 + (tl.dx ? ac : al);
+        if (i >= 0 && j >= 0 && i < lat && j < lat && j >= jlo && j <= jhi)
+          v = x[(comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i];
+      } else {
+        const int r = q - NXS, ac = r / (T + 4), al = r % (T + 4);
+        const int kx = tl.kx - 2 + (tl.dx ? al : ac), ky = tl.ky - 2 + (tl.dx ? ac : al);
+        if (kx >= 0 && ky >= 0 && kx <= N && ky <= N && 2 * ky >= jlo && 2 * ky <= jhi) v = x[p_at(g, kx, ky)];
+      }
+      xs[q] = v;
+    }
+    __syncthreads();
+  }
+  auto XS = [&](int comp, int i, int j) -> double {
+    const int ai = i - (i0 - 2), aj = j - (j0 - 2);
+    return xs[comp * 9 * kBdStA + (tl.dx ? aj * kBdStA + ai : ai * kBdStA + aj)];
+  };
+  auto PS = [&](int kx, int ky) -> double {
+    const int ax = kx - (tl.kx - 2), ay = ky - (tl.ky - 2);
+    return xs[NXS + (tl.dx ? ay * (T + 4) + ax : ax * (T + 4) + ay)];
+  };
   for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
     double r = 0.0;
     if (q < NBAND) {
@@ -307,12 +350,12 @@ __global__ void __launch_bounds__(kBdThreads) k_boundary_patches(LevelGeom g, do
       if (al < nalong && jslab && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
         const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
         double ax = 0.0;
-        if (x) ax = nu * lap_at(x + (comp ? g.ouy : g.oux), g.pu, i, j) + gradp_at(x + g.op, g.pp, i, j, comp, g.h);
+        if (x) ax = nu * lap_f([&](int ii, int jj) { return XS(comp, ii, jj); }, i, j) + gradp_f(PS, i, j, comp, g.h);
         r = b[o] - ax;
       }
     } else if (q - NBAND < tl.n && tl.ky + (q - NBAND) * tl.dy >= g.r0 - 1 && tl.ky + (q - NBAND) * tl.dy <= g.r1) {
       const int pi = q - NBAND, kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
-      const double ax = x ? div_at(x + g.oux, x + g.ouy, g.pu, N, kx, ky, g.h) : 0.0;
+      const double ax = x ? div_f(XS, N, kx, ky, g.h) : 0.0;
       r = b[p_at(g, kx, ky)] - ax;
     }
     band[q] = r;
@@ -1216,8 +1259,11 @@ inline bool make_p_map(CUtensorMap* m, const LevelGeom& g, const double* v, unsi
 
 inline int launch_fused_sweep(const LevelGeom& g, double nu, double omega, int scalar_w, const FusedFactors& F,
                               const double* dinv, const BdTile* tiles, int ntiles, double* bd, const double* xin,
-                              const double* b, double* xout, int nsm, cudaStream_t s) {
+                              const double* b, double* xout, int nsm, cudaStream_t s, cudaEvent_t ev0 = nullptr,
+                              unsigned ev0_flags = 0) {
   launch_pdl(k_boundary_patches, dim3((unsigned)ntiles), dim3(kBdThreads), 0, s, g, nu, dinv, tiles, xin, b, bd);
+  // profiling: the caller's start event between the two kernels times the sweep kernel alone
+  if (ev0 && cudaEventRecordWithFlags(ev0, s, ev0_flags) != cudaSuccess) return -3;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
