@@ -229,9 +229,10 @@ __global__ void k_factor_setup(const int* __restrict__ Ns, double nu, double* __
 // Boundary patches (some axis category != 2: kx or ky in {0, 1, N-1, N}).
 // They are only O(N) of the (N+1)^2 patches but have 24 different matrices
 // without the reflection symmetry, so they are solved up front by this small
-// kernel -- one CTA of 64 threads per patch: the 51 window residuals
-// (stencil from global memory), then one row of the dense padded group
-// inverse per thread -- and their corrections are stored slot-major in `bd`.
+// kernel -- one CTA of 256 threads per tile of 16 patches of one group: the
+// window residuals on the tile's band, then the dense padded group inverse
+// applied on the FP64 tensor path -- and their corrections are stored
+// slot-major in `bd`.
 // The fused kernel then loads them instead of diverging into a dense solve.
 // Boundary patch numbering: rows ky in {0,1,N-1,N} first (4 x (N+1)), then
 // columns kx in {0,1,N-1,N} for 2 <= ky <= N-2 (4 x (N-3)); nb = 8N - 8.
@@ -255,9 +256,9 @@ struct BdTile {
 #define SVK_BD_TILE 16
 #endif
 #ifndef SVK_BD_MINB
-#define SVK_BD_MINB 1
+#define SVK_BD_MINB 3
 #endif
-constexpr int kBdTile = SVK_BD_TILE, kBdThreads = 512;
+constexpr int kBdTile = SVK_BD_TILE, kBdThreads = 256;
 inline std::vector<BdTile> make_bd_tiles(int N) {
   std::vector<BdTile> t;
   auto seg = [&](int kx, int ky, int dx, int dy, int n) {
@@ -285,19 +286,31 @@ inline std::vector<BdTile> make_bd_tiles(int N) {
 // per component, 5 x (n+4) pressure nodes) is first staged in shared memory, so
 // that each x value is read from memory once instead of by every stencil that
 // touches it (the residual then uses lap_f / gradp_f / div_f on the stage, the
-// same arithmetic as lap_at / gradp_at / div_at).
+// same arithmetic as lap_at / gradp_at / div_at).  Every global load of the tile
+// (group inverse, x stage, b on the band) is issued in one phase.
+// Phase 3 is a small dense contraction, D[p][s] = sum_c R[p][c] Ai[s][c] (16
+// patches x 51 slots x 51), run on the FP64 tensor path: mma.sync m8n8k4 f64
+// (DMMA), patches along M (2 tiles), slots along N (7 tiles, one per warp),
+// slots along K (13 steps), fragments read straight from shared memory.
 constexpr int kBdBandW = 2 * kBdTile + 3;  // band length along the tile
 constexpr int kBdStA = kBdBandW + 4;       // staged length along (stencil halo 2 + 2)
+static_assert(kBdTile == 16, "the DMMA apply tiles 16 patches as two m8 tiles");
+static_assert(kBdThreads >= 7 * 32, "one warp per n8 tile of the 51 slots");
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(LevelGeom g, double nu, const double* __restrict__ dinv,
                                                          const BdTile* __restrict__ tiles,
                                                          const double* __restrict__ x, const double* __restrict__ b,
                                                          double* __restrict__ bd) {
-  constexpr int T = kBdTile, RS = 53;  // odd row stride: conflict-free 64-bit smem accesses
+  constexpr int T = kBdTile, RS = 53;  // odd row stride: few bank conflicts on the fragment loads
   constexpr int NBAND = 2 * 5 * kBdBandW;
   constexpr int NXS = 2 * 9 * kBdStA, NPS = 5 * (T + 4);
   __shared__ double Ai[kGroupStride];
   __shared__ double rv[T * RS];
-  __shared__ double band[NBAND + T];  // [comp][5 across][kBdBandW along] + pressure residuals
+  __shared__ double band[NBAND + T];  // [comp][5 across][kBdBandW along] + pressure residuals (b first)
   __shared__ double xs[NXS + NPS];    // x != 0: [comp][9 across][kBdStA along] + [5 across][T + 4 along]
   pdl_wait();
   const int N = g.N, lat = g.lat;
@@ -306,7 +319,6 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
   const int ylo = tl.ky + (tl.n - 1) * tl.dy;
   if (max(tl.ky, ylo) < g.r0 - 1 || min(tl.ky, ylo) > g.r1) return;  // patch rows a slab uses: r0-1 .. r1
   const double* A = dinv + (size_t)tl.grp * kGroupStride;
-  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) Ai[q] = A[q];
   // band origin: lattice point (2 kx - 2, 2 ky - 2) of the tile's first patch; "along" = tile direction
   const int i0 = 2 * tl.kx - 2, j0 = 2 * tl.ky - 2;
   const int nalong = 2 * tl.n + 3;
@@ -314,6 +326,8 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
   // Rows a slab-local vector does not hold are never read by the band's stencils
   // (the stencils of band rows outside the slab's patch rows are skipped below).
   const int jlo = 2 * (g.r0 - 1) - 4, jhi = 2 * g.r1 + 4;
+  // ---- phase 0: every global load of the tile ----
+  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) Ai[q] = A[q];
   if (x) {
     for (int q = threadIdx.x; q < NXS + NPS; q += blockDim.x) {
       double v = 0.0;
@@ -329,38 +343,57 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
       }
       xs[q] = v;
     }
-    __syncthreads();
   }
-  auto XS = [&](int comp, int i, int j) -> double {
-    const int ai = i - (i0 - 2), aj = j - (j0 - 2);
-    return xs[comp * 9 * kBdStA + (tl.dx ? aj * kBdStA + ai : ai * kBdStA + aj)];
-  };
-  auto PS = [&](int kx, int ky) -> double {
-    const int ax = kx - (tl.kx - 2), ay = ky - (tl.ky - 2);
-    return xs[NXS + (tl.dx ? ay * (T + 4) + ax : ax * (T + 4) + ay)];
+  // b on the band (0 where the residual is not formed: Dirichlet / outside / beyond the slab)
+  auto band_ij = [&](int q, int& comp, int& i, int& j, bool& ok) {
+    comp = q / (5 * kBdBandW);
+    const int rem = q % (5 * kBdBandW), ac = rem / kBdBandW, al = rem % kBdBandW;
+    i = i0 + (tl.dx ? al : ac);
+    j = j0 + (tl.dx ? ac : al);
+    // only rows of the patches this slab solves (ky in r0-1 .. r1): a column
+    // tile may reach beyond them, and a slab-local vector holds no rows there
+    const bool jslab = j >= 2 * (g.r0 - 1) - 2 && j <= 2 * g.r1 + 2;
+    ok = al < nalong && jslab && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2;
   };
   for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
-    double r = 0.0;
+    double v = 0.0;
     if (q < NBAND) {
-      const int comp = q / (5 * kBdBandW), rem = q % (5 * kBdBandW), ac = rem / kBdBandW, al = rem % kBdBandW;
-      const int i = i0 + (tl.dx ? al : ac), j = j0 + (tl.dx ? ac : al);
-      // only rows of the patches this slab solves (ky in r0-1 .. r1): a column
-      // tile may reach beyond them, and a slab-local vector holds no rows there
-      const bool jslab = j >= 2 * (g.r0 - 1) - 2 && j <= 2 * g.r1 + 2;
-      if (al < nalong && jslab && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2) {
-        const int64_t o = (comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-        double ax = 0.0;
-        if (x) ax = nu * lap_f([&](int ii, int jj) { return XS(comp, ii, jj); }, i, j) + gradp_f(PS, i, j, comp, g.h);
-        r = b[o] - ax;
-      }
+      int comp, i, j;
+      bool ok;
+      band_ij(q, comp, i, j, ok);
+      if (ok) v = b[(comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i];
     } else if (q - NBAND < tl.n && tl.ky + (q - NBAND) * tl.dy >= g.r0 - 1 && tl.ky + (q - NBAND) * tl.dy <= g.r1) {
-      const int pi = q - NBAND, kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
-      const double ax = x ? div_f(XS, N, kx, ky, g.h) : 0.0;
-      r = b[p_at(g, kx, ky)] - ax;
+      const int pi = q - NBAND;
+      v = b[p_at(g, tl.kx + pi * tl.dx, tl.ky + pi * tl.dy)];
     }
-    band[q] = r;
+    band[q] = v;
+  }
+  // ---- phase 1: r = b - A x on the band ----
+  if (x) {
+    __syncthreads();
+    auto XS = [&](int comp, int i, int j) -> double {
+      const int ai = i - (i0 - 2), aj = j - (j0 - 2);
+      return xs[comp * 9 * kBdStA + (tl.dx ? aj * kBdStA + ai : ai * kBdStA + aj)];
+    };
+    auto PS = [&](int kx, int ky) -> double {
+      const int ax = kx - (tl.kx - 2), ay = ky - (tl.ky - 2);
+      return xs[NXS + (tl.dx ? ay * (T + 4) + ax : ax * (T + 4) + ay)];
+    };
+    for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
+      if (q < NBAND) {
+        int comp, i, j;
+        bool ok;
+        band_ij(q, comp, i, j, ok);
+        if (ok)
+          band[q] -= nu * lap_f([&](int ii, int jj) { return XS(comp, ii, jj); }, i, j) + gradp_f(PS, i, j, comp, g.h);
+      } else if (q - NBAND < tl.n && tl.ky + (q - NBAND) * tl.dy >= g.r0 - 1 && tl.ky + (q - NBAND) * tl.dy <= g.r1) {
+        const int pi = q - NBAND;
+        band[q] -= div_f(XS, N, tl.kx + pi * tl.dx, tl.ky + pi * tl.dy, g.h);
+      }
+    }
   }
   __syncthreads();
+  // ---- phase 2: per-patch windows R[p][slot] ----
   for (int q = threadIdx.x; q < T * kSlots; q += blockDim.x) {
     const int pi = q % T, s = q / T;
     double r = 0.0;
@@ -376,17 +409,31 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
     rv[pi * RS + s] = r;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < T * kSlots; q += blockDim.x) {
-    const int pi = q % T, s = q / T;
-    if (pi >= tl.n) continue;
-    const int kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
-    if (ky < g.r0 - 1 || ky > g.r1) continue;
-    const double* Ar = Ai + s * kSlots;
-    const double* rr = rv + pi * RS;
-    double d = 0.0;
-    for (int c = 0; c < kSlots; ++c) d = fma(Ar[c], rr[c], d);
-    bd[(int64_t)s * nb + bd_index(kx, ky, N)] = d;
+  // ---- phase 3: D = R Ai^T on DMMA; warp w computes slots 8w .. 8w+7 of all 16 patches ----
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= 7) return;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const int sb = 8 * warp + gq;  // B fragment: B[k][n] = Ai[n][k], n = slot 8w + (lane >> 2)
+  double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kt = 0; kt < 13; ++kt) {
+    const int c = 4 * kt + t4;  // K index (slot of the residual window)
+    const double bfr = (sb < kSlots && c < kSlots) ? Ai[sb * kSlots + c] : 0.0;
+    const double a0 = c < kSlots ? rv[gq * RS + c] : 0.0;        // A[m][k] = R[patch gq][c]
+    const double a1 = c < kSlots ? rv[(8 + gq) * RS + c] : 0.0;  // patches 8 + gq
+    dmma_m8n8k4(d[0][0], d[0][1], a0, bfr);
+    dmma_m8n8k4(d[1][0], d[1][1], a1, bfr);
   }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int pi = 8 * mt + gq, s = 8 * warp + 2 * t4 + jj;  // C[m][n]: m = patch, n = slot
+      if (pi >= tl.n || s >= kSlots) continue;
+      const int kx = tl.kx + pi * tl.dx, ky = tl.ky + pi * tl.dy;
+      if (ky < g.r0 - 1 || ky > g.r1) continue;
+      bd[(int64_t)s * nb + bd_index(kx, ky, N)] = d[mt][jj];
+    }
 }
 
 // =============================================================================
