@@ -21,6 +21,7 @@
 #include "kernels_common.cuh"
 #include "krylov.cuh"
 #include "sweep_fused.cuh"
+#include "small_cycle.cuh"
 #include "residual_strip.cuh"
 #include "relax_bs.cuh"
 #include "bt.cuh"
@@ -46,6 +47,12 @@ struct svk_ctx {
   double* d_dbuf = nullptr;  // packed patch buffer (unfused sweep), finest-level size
   std::vector<double*> d_inv_simple;  // SIMPLE: per level, every patch's inverse (slot-interleaved)
   double* d_bd = nullptr;    // boundary-patch corrections (fused sweep), finest-level size
+  // coarse-level V-cycle in one cluster launch (small_cycle.cuh): levels 1 .. sc_top
+  // (N <= SVK_SMALL_N, below the finest level, replicated), sc_cluster CTAs
+  int sc_top = 0, sc_cluster = 0;
+  double* d_sc = nullptr;  // patch corrections of the largest small level, slot-major
+  std::vector<BdTile*> d_sc_tiles;  // per small level: every patch in tiles of one group
+  std::vector<int> n_sc_tiles;
   std::vector<BdTile*> d_tiles;  // per level: boundary-patch tiles (k_boundary_patches)
   std::vector<int> ntiles;
   double* d_sw = nullptr;    // extra ping-pong vector for nsweeps > 1, finest-level size
@@ -823,9 +830,124 @@ int op_agglomerate(svk_ctx* ctx, int l, double* rc, cudaStream_t s) {
 // agglomeration level the restricted residual is assembled on every rank by an
 // all-reduce of the disjoint, zero-padded slab pieces; the coarser levels then
 // run redundantly (replicated) on every rank.
+// Which coarse levels run in the one-launch V-cycle, and on how many CTAs.
+// SVK_SMALL_N (default 16, measured best: 4096^2 V-cycle 5378 -> 5341 us, 1024^2
+// 859 -> 813 us; at 32 / 64 the grid-stride phases of the larger levels cost
+// more than the launches they replace): largest N; 0 disables.  Only the fused Vanka
+// relaxation, only replicated levels below the finest.  Cluster: 16 CTAs
+// (non-portable size) when the device can co-schedule it, else 8.
+int setup_small_cycle(svk_ctx* ctx) {
+  ctx->sc_top = 0;
+  const char* e = std::getenv("SVK_SMALL_N");
+  const int lc = e ? std::atoi(e) : 16;
+  const svk_config& c = ctx->cfg;
+  if (lc <= 0 || c.relax != SVK_RELAX_VANKA || c.sweep_impl != SVK_SWEEP_FUSED) return SVK_OK;
+  int top = 0;
+  for (int l = 1; l < ctx->nlev - 1 && l < kScMaxLevels; ++l)
+    if (ctx->g[l].N <= lc && !dist_level(ctx, l)) top = l;
+  if (top < 1) return SVK_OK;
+  CK(cudaFuncSetAttribute(k_small_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const char* ce = std::getenv("SVK_SMALL_CLUSTER");
+  int cl = ce ? std::atoi(ce) : 16;
+  for (; cl >= 1; cl /= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cl);
+    cfg.blockDim = dim3(kScThreads);
+      cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_small_cycle, &cfg) == cudaSuccess && n >= 1) break;
+    cudaGetLastError();
+  }
+  if (cl < 1) return SVK_OK;
+  const int64_t np = (int64_t)(ctx->g[top].N + 1) * (ctx->g[top].N + 1);
+  TRY(alloc_vec(ctx, &ctx->d_sc, (int64_t)kSlots * np));
+  for (int l = 0; l <= top; ++l) {  // boundary tiles + the generic patches in row segments of <= kBdTile
+    const int N = ctx->g[l].N;
+    std::vector<BdTile> t = make_bd_tiles(N);
+    for (int ky = 2; ky <= N - 2; ++ky)
+      for (int kx = 2; kx <= N - 2; kx += kBdTile)
+        t.push_back(BdTile{kx, ky, 1, 0, std::min(kBdTile, N - 1 - kx), 2 * 5 + 2});
+    BdTile* d = nullptr;
+    CK(cudaMalloc(&d, t.size() * sizeof(BdTile)));
+    CK(cudaMemcpy(d, t.data(), t.size() * sizeof(BdTile), cudaMemcpyHostToDevice));
+    ctx->d_sc_tiles.push_back(d);
+    ctx->n_sc_tiles.push_back((int)t.size());
+  }
+  ctx->sc_cluster = cl;
+  ctx->sc_top = top;
+  if (const char* d = std::getenv("SVK_DEBUG_SMALL"); d && d[0] == '1')
+    std::fprintf(stderr, "[small-cycle] levels 1..%d (N <= %d), cluster of %d CTAs\n", top, ctx->g[top].N, cl);
+  return SVK_OK;
+}
+
+// MG(l) from x = 0 on the levels l .. 0 (alg:mg) as ONE cluster launch
+// (small_cycle.cuh): same steps and operators as the per-kernel recursion below.
+int op_small_cycle(svk_ctx* ctx, int l, const double* b, double* x, cudaStream_t s) {
+  ScArgs a{};
+  a.top = l;
+  for (int k = 0; k <= l; ++k) {
+    ScLevel& L = a.lv[k];
+    L.g = ctx->g[k];
+    L.dinv = ctx->d_inv + (size_t)k * 25 * kGroupStride;
+    L.tiles = ctx->d_sc_tiles[k];
+    L.ntiles = ctx->n_sc_tiles[k];
+    L.b = k == l ? const_cast<double*>(b) : ctx->ws_b[k];
+    L.x = k == l ? x : ctx->ws_x[k];
+    L.r = ctx->ws_r[k];
+  }
+  const svk_config& c = ctx->cfg;
+  a.nu = c.nu;
+  a.omega = c.omega_v;
+  a.scalar_w = c.weighting == SVK_WEIGHT_SCALAR;
+  a.nu_pre = c.nu_pre;
+  a.nu_post = c.nu_post;
+  a.sweeps3 = c.coarse == SVK_COARSE_SWEEPS3;
+  a.cmat = ctx->d_cmat;
+  a.cidx = ctx->d_cidx;
+  a.cni = ctx->cni;
+  a.d = ctx->d_sc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ctx->sc_cluster);
+  cfg.blockDim = dim3(kScThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)ctx->sc_cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const char* dbg = std::getenv("SVK_DEBUG_SMALL");
+  static unsigned long long* stamps = nullptr;  // development aid only (run with SVK_GRAPHS=0)
+  if (dbg && dbg[0] == '2') {
+    if (!stamps) CK(cudaMallocManaged(&stamps, 4096 * sizeof(unsigned long long)));
+    a.stamps = stamps;
+  }
+  CK(cudaLaunchKernelEx(&cfg, k_small_cycle, a));
+  if (a.stamps) {
+    CK(cudaStreamSynchronize(s));
+    std::string o = "[small-cycle us]";
+    for (int k = 1; k < 4096 && stamps[k] > stamps[k - 1] && stamps[k] - stamps[0] < 100000000ull; ++k)
+      o += " " + std::to_string((stamps[k] - stamps[k - 1]) / 100 / 10.0);
+    std::fprintf(stderr, "%s\n", o.c_str());
+    std::memset(stamps, 0, 4096 * sizeof(unsigned long long));
+  }
+  ctx->launches++;
+  return SVK_OK;
+}
+
 int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStream_t s) {
   const LevelGeom& g = ctx->g[l];
   if (l == 0) return op_coarse(ctx, b, x, s);
+  if (x_zero && l <= ctx->sc_top) return op_small_cycle(ctx, l, b, x, s);  // levels l .. 0 in one launch
   const bool D = dist_level(ctx, l);
   if (D) {
     TRY(op_halo(ctx, l, const_cast<double*>(b), s));
@@ -1250,6 +1372,8 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_dbuf);
   for (double* p : ctx->d_inv_simple) F(p);
   F(ctx->d_bd);
+  F(ctx->d_sc);
+  for (BdTile* p : ctx->d_sc_tiles) F(p);
   for (BdTile* p : ctx->d_tiles) F(p);
   free_vec(ctx, ctx->d_sw);
   F(ctx->d_schur);
@@ -1405,6 +1529,7 @@ int create_impl(svk_ctx* ctx) {
     ctx->ntiles.push_back((int)t.size());
     CK(cudaMemcpy(d, t.data(), t.size() * sizeof(BdTile), cudaMemcpyHostToDevice));
   }
+  TRY(setup_small_cycle(ctx));
   if (c.sweep_impl == SVK_SWEEP_SIMPLE) {  // simple Vanka: build and store every patch's inverse
     int* d_st;
     CK(cudaMalloc(&d_st, sizeof(int)));
