@@ -379,13 +379,54 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
       const int ax = kx - (tl.kx - 2), ay = ky - (tl.ky - 2);
       return xs[NXS + (tl.dx ? ay * (T + 4) + ax : ax * (T + 4) + ay)];
     };
+    // stage strides: lattice (i, j) -> xs[comp * 9 kBdStA + (i - i0 + 2) si + (j - j0 + 2) sj]
+    const int si = tl.dx ? 1 : kBdStA, sj = tl.dx ? kBdStA : 1;
+    const int pxs = tl.dx ? 1 : T + 4, pys = tl.dx ? T + 4 : 1;  // pressure stage strides
     for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
       if (q < NBAND) {
         int comp, i, j;
         bool ok;
         band_ij(q, comp, i, j, ok);
-        if (ok)
-          band[q] -= nu * lap_f([&](int ii, int jj) { return XS(comp, ii, jj); }, i, j) + gradp_f(PS, i, j, comp, g.h);
+        if (ok) {
+          // (L u + B^T p)(i, j) with the whole 5x5 / 3x3 stage windows read first: the
+          // products and summation order of lap_f / gradp_f; the taps lap_f skips (odd
+          // parity, offsets +-2) carry the exact zeros KR[1][0,4] = MR[1][0,4] = 0
+          const int pi = i & 1, pj = j & 1;
+          const double* xc = xs + comp * 9 * kBdStA + (i - i0 + 2) * si + (j - j0 + 2) * sj;
+          double U[5][5];
+#pragma unroll
+          for (int bb = 0; bb < 5; ++bb)
+#pragma unroll
+            for (int aa = 0; aa < 5; ++aa) U[bb][aa] = xc[(aa - 2) * si + (bb - 2) * sj];
+          const int ky0 = pj ? (j - 1) >> 1 : (j >> 1) - 1, nky = pj ? 2 : 3;
+          const int kx0 = pi ? (i - 1) >> 1 : (i >> 1) - 1, nkx = pi ? 2 : 3;
+          const double* pc = xs + NXS + (kx0 - (tl.kx - 2)) * pxs + (ky0 - (tl.ky - 2)) * pys;
+          double P[3][3];
+#pragma unroll
+          for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+            for (int tx = 0; tx < 3; ++tx) P[ty][tx] = pc[min(tx, nkx - 1) * pxs + min(ty, nky - 1) * pys];
+          double sl = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < 5; ++bb) {
+            const double my = c_st.MR[pj][bb], ky = c_st.KR[pj][bb];
+#pragma unroll
+            for (int aa = 0; aa < 5; ++aa) sl += (my * c_st.KR[pi][aa] + ky * c_st.MR[pi][aa]) * U[bb][aa];
+          }
+          double sp = 0.0;
+#pragma unroll
+          for (int ty = 0; ty < 3; ++ty) {
+            if (ty >= nky) continue;
+            const double cy = comp == 0 ? c_st.CC[pj][ty] : c_st.GC[pj][ty];
+            if (cy == 0.0) continue;
+            double t = 0.0;
+#pragma unroll
+            for (int tx = 0; tx < 3; ++tx)
+              if (tx < nkx) t += (comp == 0 ? c_st.GC[pi][tx] : c_st.CC[pi][tx]) * P[ty][tx];
+            sp += cy * t;
+          }
+          band[q] -= nu * sl + -g.h * sp;
+        }
       } else if (q - NBAND < tl.n && tl.ky + (q - NBAND) * tl.dy >= g.r0 - 1 && tl.ky + (q - NBAND) * tl.dy <= g.r1) {
         const int pi = q - NBAND;
         band[q] -= div_f(XS, N, tl.kx + pi * tl.dx, tl.ky + pi * tl.dy, g.h);
