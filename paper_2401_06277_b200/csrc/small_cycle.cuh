@@ -52,7 +52,7 @@ struct ScArgs {
   unsigned long long* stamps;  // development aid (SVK_DEBUG_SMALL=2): %globaltimer after each barrier
 };
 
-__device__ __noinline__ void sc_sync() {
+__device__ __forceinline__ void sc_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ unsigned sc_rank() {
@@ -70,6 +70,14 @@ __device__ __forceinline__ unsigned sc_ncta() {
 // cluster barrier's acquire invalidates the L1 (CCTL.IVALL in the SASS)
 #define LDX(p) (*(p))
 
+// the 1D stencil rows the residual needs, copied from c_st into shared memory at
+// kernel start: the lanes of a warp index them by their own lattice parity, and
+// divergent __constant__ reads serialise (each distinct address is a separate
+// constant-cache access, a miss an L2 round trip)
+struct ScStencil {
+  double KR[2][5], MR[2][5], CC[2][3], GC[2][3], CR[3][5], GR[3][5];
+};
+
 struct ScThreads {
   int gt, nt;  // cluster-wide thread index / count
   int gw, nw;  // cluster-wide warp index / count
@@ -81,7 +89,8 @@ struct ScThreads {
 // products and summation order as lap_at / gradp_at: the taps lap_at skips (odd
 // parity: offsets +-2) carry the exact zeros KR[1][0,4] = MR[1][0,4] = 0, so the
 // sum is bitwise the same; their clamped loads only keep addresses in range.
-__device__ __forceinline__ double sc_ax_vel(const LevelGeom& g, double nu, const double* x, int plane, int i, int j) {
+__device__ __forceinline__ double sc_ax_vel(const LevelGeom& g, const ScStencil& cs, double nu, const double* x, int plane,
+                                            int i, int j) {
   const int pi = i & 1, pj = j & 1, lat = g.lat;
   const double* u = x + (plane ? g.ouy : g.oux);
   double U[5][5];
@@ -103,26 +112,26 @@ __device__ __forceinline__ double sc_ax_vel(const LevelGeom& g, double nu, const
   double s = 0.0;
 #pragma unroll
   for (int bb = 0; bb < 5; ++bb) {
-    const double my = c_st.MR[pj][bb], ky = c_st.KR[pj][bb];
+    const double my = cs.MR[pj][bb], ky = cs.KR[pj][bb];
 #pragma unroll
-    for (int aa = 0; aa < 5; ++aa) s += (my * c_st.KR[pi][aa] + ky * c_st.MR[pi][aa]) * U[bb][aa];
+    for (int aa = 0; aa < 5; ++aa) s += (my * cs.KR[pi][aa] + ky * cs.MR[pi][aa]) * U[bb][aa];
   }
   double sp = 0.0;
 #pragma unroll
   for (int ty = 0; ty < 3; ++ty) {
     if (ty >= nky) continue;
-    const double cy = plane == 0 ? c_st.CC[pj][ty] : c_st.GC[pj][ty];
+    const double cy = plane == 0 ? cs.CC[pj][ty] : cs.GC[pj][ty];
     if (cy == 0.0) continue;
     double t = 0.0;
 #pragma unroll
     for (int tx = 0; tx < 3; ++tx)
-      if (tx < nkx) t += (plane == 0 ? c_st.GC[pi][tx] : c_st.CC[pi][tx]) * P[ty][tx];
+      if (tx < nkx) t += (plane == 0 ? cs.GC[pi][tx] : cs.CC[pi][tx]) * P[ty][tx];
     sp += cy * t;
   }
   return nu * s + -g.h * sp;
 }
 // (B u)(kx, ky) with the 5x5 windows of both components loaded up front (div_at order)
-__device__ __forceinline__ double sc_ax_p(const LevelGeom& g, const double* x, int kx, int ky) {
+__device__ __forceinline__ double sc_ax_p(const LevelGeom& g, const ScStencil& cs, const double* x, int kx, int ky) {
   const int N = g.N, lat = g.lat;
   const int cx = kx == 0 ? 0 : (kx == N ? 2 : 1), cy = ky == 0 ? 0 : (ky == N ? 2 : 1);
   double U[5][5], V[5][5];
@@ -142,47 +151,59 @@ __device__ __forceinline__ double sc_ax_p(const LevelGeom& g, const double* x, i
   for (int oy = 0; oy < 5; ++oy) {
     const int j = 2 * ky - 2 + oy;
     if (j < 0 || j >= lat) continue;
-    const double cyc = c_st.CR[cy][oy], gyc = c_st.GR[cy][oy];
+    const double cyc = cs.CR[cy][oy], gyc = cs.GR[cy][oy];
 #pragma unroll
     for (int ox = 0; ox < 5; ++ox) {
       const int i = 2 * kx - 2 + ox;
       if (i < 0 || i >= lat) continue;
-      s += cyc * c_st.GR[cx][ox] * U[oy][ox] + gyc * c_st.CR[cx][ox] * V[oy][ox];
+      s += cyc * cs.GR[cx][ox] * U[oy][ox] + gyc * cs.CR[cx][ox] * V[oy][ox];
     }
   }
   return -g.h * s;
 }
 
-// r = b - A x (x == nullptr: r = b), masked to 0 on Dirichlet rows and padding (k_residual)
-__device__ __noinline__ void sc_residual(const ScLevel& L, double nu, const double* x, double* r, const ScThreads& T) {
-  const LevelGeom& g = L.g;
-  const int N = g.N, lat = g.lat;
-  const int64_t nvel = (int64_t)lat * g.pu;
-  const int64_t total = 2 * nvel + (int64_t)(N + 1) * g.pp;
-  for (int64_t q = T.gt; q < total; q += T.nt) {
-    if (q < 2 * nvel) {
-      const int plane = q >= nvel ? 1 : 0;
-      const int64_t qq = q - plane * nvel;
-      const int j = (int)(qq / g.pu), i = (int)(qq % g.pu);
-      const int64_t o = (plane ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-      if (i >= lat || i == 0 || j == 0 || i == lat - 1 || j == lat - 1) {
-        r[o] = 0.0;
-        continue;
-      }
-      const double bo = L.b[o];
-      r[o] = x ? bo - sc_ax_vel(g, nu, x, plane, i, j) : bo;
+// every entry of a level vector: one warp per lattice / pressure row, lanes along
+// the row (no 64-bit index division), fv(plane, j, i, offset) / fp(j, i, offset)
+template <class Fv, class Fp>
+__device__ __forceinline__ void sc_for_points(const LevelGeom& g, const ScThreads& T, Fv fv, Fp fp) {
+  const int nrows = 2 * g.lat + g.N + 1;
+  for (int row = T.gw; row < nrows; row += T.nw) {
+    if (row < 2 * g.lat) {
+      const int plane = row >= g.lat ? 1 : 0, j = row - plane * g.lat;
+      const int64_t base = (plane ? g.ouy : g.oux) + (int64_t)j * g.pu;
+      for (int i = T.lane; i < g.pu; i += 32) fv(plane, j, i, base + i);
     } else {
-      const int64_t qq = q - 2 * nvel;
-      const int j = (int)(qq / g.pp), i = (int)(qq % g.pp);
-      const int64_t o = g.op + (int64_t)j * g.pp + i;
-      if (i > N) {
-        r[o] = 0.0;
-        continue;
-      }
-      const double bo = L.b[o];
-      r[o] = x ? bo - sc_ax_p(g, x, i, j) : bo;
+      const int j = row - 2 * g.lat;
+      const int64_t base = g.op + (int64_t)j * g.pp;
+      for (int i = T.lane; i < g.pp; i += 32) fp(j, i, base + i);
     }
   }
+}
+
+// r = b - A x (x == nullptr: r = b), masked to 0 on Dirichlet rows and padding (k_residual)
+__device__ __noinline__ void sc_residual(const ScLevel& L, const ScStencil& cs, double nu, const double* x, double* r,
+                                         const ScThreads& T) {
+  const LevelGeom g = L.g;
+  const double* b = L.b;
+  const int N = g.N, lat = g.lat;
+  sc_for_points(
+      g, T,
+      [&](int plane, int j, int i, int64_t o) {
+        if (i >= lat || i == 0 || j == 0 || i == lat - 1 || j == lat - 1) {
+          r[o] = 0.0;
+          return;
+        }
+        const double bo = b[o];
+        r[o] = x ? bo - sc_ax_vel(g, cs, nu, x, plane, i, j) : bo;
+      },
+      [&](int j, int i, int64_t o) {
+        if (i > N) {
+          r[o] = 0.0;
+          return;
+        }
+        const double bo = b[o];
+        r[o] = x ? bo - sc_ax_p(g, cs, x, i, j) : bo;
+      });
 }
 
 // delta_i = A_i^{-1} V_i r for every patch of the level, slot-major into d: one
@@ -254,120 +275,114 @@ __device__ __noinline__ void sc_patches(const ScLevel& L, const double* r, doubl
 
 // x_out = x_in + W sum_i V_i^T delta_i, in place (k_vanka_update; xzero: x_in = 0)
 __device__ __noinline__ void sc_update(const ScLevel& L, double omega, int scalar_w, bool xzero, const double* d,
-                          const ScThreads& T) {
-  const LevelGeom& g = L.g;
+                                       const ScThreads& T) {
+  const LevelGeom g = L.g;
   const int N = g.N, lat = g.lat;
   const int64_t np = (int64_t)(N + 1) * (N + 1);
-  const int64_t nvel = (int64_t)lat * g.pu;
-  const int64_t total = 2 * nvel + (int64_t)(N + 1) * g.pp;
   double* x = L.x;
-  for (int64_t q = T.gt; q < total; q += T.nt) {
-    if (q < 2 * nvel) {
-      const int plane = q >= nvel ? 1 : 0;
-      const int64_t qq = q - plane * nvel;
-      const int j = (int)(qq / g.pu), i = (int)(qq % g.pu);
-      const int64_t o = (plane ? g.ouy : g.oux) + (int64_t)j * g.pu + i;
-      if (i >= lat) {
-        x[o] = 0.0;
-        continue;
-      }
-      const double xin = xzero ? 0.0 : LDX(x + o);
-      if (i == 0 || j == 0 || i == lat - 1 || j == lat - 1) {
-        x[o] = xin;
-        continue;
-      }
-      const int kx0 = max(0, (i - 1) >> 1), kx1 = min(N, (i + 2) >> 1);
-      const int ky0 = max(0, (j - 1) >> 1), ky1 = min(N, (j + 2) >> 1);
-      double v[3][3];  // all loads first, then the sum in the k_vanka_update order
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int ky = ky0 + a, kx = kx0 + c;
-          const int slot = plane * 25 + (j - 2 * ky + 2) * 5 + (i - 2 * kx + 2);
-          const bool in = ky <= ky1 && kx <= kx1;
-          v[a][c] = LDX(d + (in ? (int64_t)slot * np + (int64_t)ky * (N + 1) + kx : 0));  // unused: skipped below
+  sc_for_points(
+      g, T,
+      [&](int plane, int j, int i, int64_t o) {
+        if (i >= lat) {
+          x[o] = 0.0;
+          return;
         }
-      double s = 0.0;
+        const double xin = xzero ? 0.0 : LDX(x + o);
+        if (i == 0 || j == 0 || i == lat - 1 || j == lat - 1) {
+          x[o] = xin;
+          return;
+        }
+        const int kx0 = max(0, (i - 1) >> 1), kx1 = min(N, (i + 2) >> 1);
+        const int ky0 = max(0, (j - 1) >> 1), ky1 = min(N, (j + 2) >> 1);
+        double v[3][3];  // all loads first, then the sum in the k_vanka_update order
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (ky0 + a <= ky1 && kx0 + c <= kx1) s += v[a][c];
-      const int mult = (kx1 - kx0 + 1) * (ky1 - ky0 + 1);
-      x[o] = xin + (scalar_w ? omega : omega / mult) * s;
-    } else {
-      const int64_t qq = q - 2 * nvel;
-      const int j = (int)(qq / g.pp), i = (int)(qq % g.pp);
-      const int64_t o = g.op + (int64_t)j * g.pp + i;
-      if (i > N) {
-        x[o] = 0.0;
-        continue;
-      }
-      const double xin = xzero ? 0.0 : LDX(x + o);
-      x[o] = xin + omega * LDX(d + 50 * np + (int64_t)j * (N + 1) + i);
-    }
-  }
+          for (int c = 0; c < 3; ++c) {
+            const int ky = ky0 + a, kx = kx0 + c;
+            const int slot = plane * 25 + (j - 2 * ky + 2) * 5 + (i - 2 * kx + 2);
+            const bool in = ky <= ky1 && kx <= kx1;
+            v[a][c] = LDX(d + (in ? (int64_t)slot * np + (int64_t)ky * (N + 1) + kx : 0));  // unused: skipped
+          }
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (ky0 + a <= ky1 && kx0 + c <= kx1) s += v[a][c];
+        const int mult = (kx1 - kx0 + 1) * (ky1 - ky0 + 1);
+        x[o] = xin + (scalar_w ? omega : omega / mult) * s;
+      },
+      [&](int j, int i, int64_t o) {
+        if (i > N) {
+          x[o] = 0.0;
+          return;
+        }
+        const double xin = xzero ? 0.0 : LDX(x + o);
+        x[o] = xin + omega * LDX(d + 50 * np + (int64_t)j * (N + 1) + i);
+      });
 }
 
 // r_c = P^T r_f, coarse Dirichlet rows and padding set to 0 (k_restrict)
-__device__ __noinline__ void sc_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* rf, double* rc, const ScThreads& T) {
-  const int64_t nvel = (int64_t)gc.lat * gc.pu;
-  const int64_t total = 2 * nvel + (int64_t)(gc.N + 1) * gc.pp;
-  for (int64_t q = T.gt; q < total; q += T.nt) {
-    if (q < 2 * nvel) {
-      const int plane = q >= nvel ? 1 : 0;
-      const int64_t qq = q - plane * nvel;
-      const int j = (int)(qq / gc.pu), i = (int)(qq % gc.pu);
-      const int64_t o = (plane ? gc.ouy : gc.oux) + (int64_t)j * gc.pu + i;
-      if (i < 1 || j < 1 || i >= gc.lat - 1 || j >= gc.lat - 1) {
-        rc[o] = 0.0;
-        continue;
-      }
-      int fx[5], fy[5];
-      double wx[5], wy[5];
-      const int nx = p2col(i, fx, wx), ny = p2col(j, fy, wy);
-      const double* r = rf + (plane ? gf.ouy : gf.oux);
-      double v[5][5];  // all loads first, then the k_restrict order
-#pragma unroll
-      for (int b = 0; b < 5; ++b)
-#pragma unroll
-        for (int a = 0; a < 5; ++a)  // unused taps (b >= ny or a >= nx): clamped load, skipped below
-          v[b][a] = LDX(r + (int64_t)fy[min(b, ny - 1)] * gf.pu + fx[min(a, nx - 1)]);
-      double s = 0.0;
-#pragma unroll
-      for (int b = 0; b < 5; ++b) {
-        if (b >= ny) continue;
-        double t = 0.0;
-#pragma unroll
-        for (int a = 0; a < 5; ++a)
-          if (a < nx) t += wx[a] * v[b][a];
-        s += wy[b] * t;
-      }
-      rc[o] = s;
-    } else {
-      const int64_t qq = q - 2 * nvel;
-      const int j = (int)(qq / gc.pp), i = (int)(qq % gc.pp);
-      const int64_t o = gc.op + (int64_t)j * gc.pp + i;
-      if (i > gc.N) {
-        rc[o] = 0.0;
-        continue;
-      }
-      const double* r = rf + gf.op;
-      double s = 0.0;
-      for (int b = -1; b <= 1; ++b) {
-        const int fj = 2 * j + b;
-        if (fj < 0 || fj > gf.N) continue;
-        const double wy = b ? 0.5 : 1.0;
-        for (int a = -1; a <= 1; ++a) {
-          const int fi = 2 * i + a;
-          if (fi < 0 || fi > gf.N) continue;
-          s += wy * (a ? 0.5 : 1.0) * LDX(r + (int64_t)fj * gf.pp + fi);
+__device__ __noinline__ void sc_restrict(const LevelGeom& gfr, const LevelGeom& gcr, const double* rf, double* rc,
+                                         const ScThreads& T) {
+  const LevelGeom gf = gfr, gc = gcr;
+  sc_for_points(
+      gc, T,
+      [&](int plane, int j, int i, int64_t o) {
+        if (i < 1 || j < 1 || i >= gc.lat - 1 || j >= gc.lat - 1) {
+          rc[o] = 0.0;
+          return;
         }
-      }
-      rc[o] = s;
-    }
-  }
+        int fx[5], fy[5];
+        double wx[5], wy[5];
+        const int nx = p2col(i, fx, wx), ny = p2col(j, fy, wy);
+        const double* r = rf + (plane ? gf.ouy : gf.oux);
+        double v[5][5];  // all loads first, then the k_restrict order
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+          for (int a = 0; a < 5; ++a)  // unused taps (b >= ny or a >= nx): clamped load, skipped below
+            v[b][a] = LDX(r + (int64_t)fy[min(b, ny - 1)] * gf.pu + fx[min(a, nx - 1)]);
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+          if (b >= ny) continue;
+          double t = 0.0;
+#pragma unroll
+          for (int a = 0; a < 5; ++a)
+            if (a < nx) t += wx[a] * v[b][a];
+          s += wy[b] * t;
+        }
+        rc[o] = s;
+      },
+      [&](int j, int i, int64_t o) {
+        if (i > gc.N) {
+          rc[o] = 0.0;
+          return;
+        }
+        const double* r = rf + gf.op;
+        double v[3][3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int a = 0; a < 3; ++a)  // fine nodes outside 0..N: clamped load, skipped below
+            v[b][a] = LDX(r + (int64_t)min(max(2 * j + b - 1, 0), gf.N) * gf.pp + min(max(2 * i + a - 1, 0), gf.N));
+        double s = 0.0;
+#pragma unroll
+        for (int b = -1; b <= 1; ++b) {
+          const int fj = 2 * j + b;
+          if (fj < 0 || fj > gf.N) continue;
+          const double wy = b ? 0.5 : 1.0;
+#pragma unroll
+          for (int a = -1; a <= 1; ++a) {
+            const int fi = 2 * i + a;
+            if (fi < 0 || fi > gf.N) continue;
+            s += wy * (a ? 0.5 : 1.0) * v[b + 1][a + 1];
+          }
+        }
+        rc[o] = s;
+      });
 }
 
 // x_f += P e_c (prolong_q2_at / prolong_q1_at with L2 loads): one unit per coarse
@@ -420,6 +435,25 @@ __device__ __noinline__ void sc_prolong(const LevelGeom& gf, const LevelGeom& gc
 }
 
 __global__ void __launch_bounds__(kScThreads, 1) k_small_cycle(const __grid_constant__ ScArgs A) {
+  __shared__ ScStencil scs;
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 2; ++a)
+      for (int k = 0; k < 5; ++k) {
+        scs.KR[a][k] = c_st.KR[a][k];
+        scs.MR[a][k] = c_st.MR[a][k];
+      }
+    for (int a = 0; a < 2; ++a)
+      for (int k = 0; k < 3; ++k) {
+        scs.CC[a][k] = c_st.CC[a][k];
+        scs.GC[a][k] = c_st.GC[a][k];
+      }
+    for (int a = 0; a < 3; ++a)
+      for (int k = 0; k < 5; ++k) {
+        scs.CR[a][k] = c_st.CR[a][k];
+        scs.GR[a][k] = c_st.GR[a][k];
+      }
+  }
+  __syncthreads();
   pdl_wait();
   ScThreads T;
   T.nt = (int)(sc_ncta() * blockDim.x);
@@ -445,7 +479,7 @@ __global__ void __launch_bounds__(kScThreads, 1) k_small_cycle(const __grid_cons
     const ScLevel& L = A.lv[l];
     const double* src = L.b;
     if (!xzero) {
-      sc_residual(L, A.nu, L.x, L.r, T);
+      sc_residual(L, scs, A.nu, L.x, L.r, T);
       src = L.r;
     }
     if (!xzero) {
@@ -467,7 +501,7 @@ __global__ void __launch_bounds__(kScThreads, 1) k_small_cycle(const __grid_cons
     stamp();
     }
     for (int k = 0; k < A.nu_pre; ++k) sweep(l, k == 0);
-    sc_residual(L, A.nu, L.x, L.r, T);
+    sc_residual(L, scs, A.nu, L.x, L.r, T);
     sc_sync();
     stamp();
     sc_restrict(L.g, A.lv[l - 1].g, L.r, A.lv[l - 1].b, T);

@@ -188,8 +188,9 @@ class Solver:
         "emulated" runs nranks logical ranks of one process on one device (one thread each).
         relax: "vanka" (the hot path), "bs" (Braess-Sarazin) or "su" (Schur-Uzawa) comparators;
         unset comparator parameters take RELAX_DEFAULTS[relax].
-        allocator: "cuda" (cudaMalloc) or "torch" (vector workspaces from torch's
-        caching allocator, svk_config.alloc_fn)."""
+        allocator: "cuda" (cudaMalloc), "torch" (vector workspaces from torch's
+        caching allocator, svk_config.alloc_fn) or an (ALLOC_FN, FREE_FN) pair of
+        the caller's ctypes callbacks."""
         import torch
         if not torch.cuda.is_available():
             raise SvkError("libsvk needs a CUDA device (B200, sm_100a); none is visible")
@@ -222,8 +223,12 @@ class Solver:
             self._alloc_cbs = torch_allocator_callbacks()
             cfg.alloc_fn = C.cast(self._alloc_cbs[0], C.c_void_p)
             cfg.free_fn = C.cast(self._alloc_cbs[1], C.c_void_p)
+        elif isinstance(allocator, tuple) and len(allocator) == 2:  # (ALLOC_FN, FREE_FN) of the caller
+            self._alloc_cbs = allocator
+            cfg.alloc_fn = C.cast(self._alloc_cbs[0], C.c_void_p)
+            cfg.free_fn = C.cast(self._alloc_cbs[1], C.c_void_p)
         elif allocator != "cuda":
-            raise SvkError("allocator must be 'cuda' or 'torch'")
+            raise SvkError("allocator must be 'cuda', 'torch' or an (ALLOC_FN, FREE_FN) pair")
         self.rank, self.nranks = rank, nranks
         self.cfg = cfg
         self.device = torch.device("cuda", device)

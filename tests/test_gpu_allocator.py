@@ -66,3 +66,45 @@ def test_report_carries_setup_time(gpu):
     rep, _, _ = solve(S)
     assert 0.0 < rep["t_setup_s"] < 60.0
     assert rep["t_total_s"] > 0.0
+
+
+def test_guarded_workspaces_no_out_of_bounds_access(gpu):
+    # Every vector workspace of the context (level vectors, boundary-patch and
+    # coarse-cycle buffers, Krylov basis) comes from an allocator that surrounds
+    # the block with 64 KB guard zones of NaN: an out-of-bounds write changes a
+    # guard (checked at free), an out-of-bounds read pulls a NaN into the result
+    # (the solve must still match the plain context bitwise).  This stands in for
+    # compute-sanitizer memcheck, which the GPU pool does not allow.
+    import ctypes as C
+
+    import torch
+    from paper_2401_06277_b200 import Solver
+    from paper_2401_06277_b200.svk import ALLOC_FN, FREE_FN
+    G = 1 << 16
+    live, bad = {}, []
+
+    def _alloc(nbytes, device, user):
+        t = torch.full(((int(nbytes) + 2 * G + 7) // 8,), float("nan"), dtype=torch.float64, device=gpu)
+        p = t.data_ptr() + G
+        live[p] = (t, int(nbytes))
+        return p
+
+    def _free(ptr, nbytes, device, user):
+        t, n = live.pop(ptr)
+        torch.cuda.synchronize()
+        g0, g1 = t[: G // 8], t[(G + n + 7) // 8:]
+        if not (bool(torch.isnan(g0).all()) and bool(torch.isnan(g1).all())):
+            bad.append(n)
+
+    cbs = (ALLOC_FN(_alloc), FREE_FN(_free))
+    for n in (32, 64, 128):
+        ref = Solver(n)
+        rep0, hist0, x0 = solve(ref)
+        ref.close()
+        S = Solver(n, allocator=cbs)
+        S.vcycle(S.set_problem("mms_paper")[0])
+        rep1, hist1, x1 = solve(S)
+        S.close()
+        assert not live and not bad, (n, bad)
+        assert rep1["iterations"] == rep0["iterations"]
+        assert np.array_equal(x0, x1)
