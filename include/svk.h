@@ -62,11 +62,17 @@
  * they compute the rank's owned rows from the rows it already holds, so the
  * caller must pass inputs whose halo rows are current (as svk_vcycle does).
  *
- * ENVIRONMENT (read once per process; tuning and test aids, results unchanged):
+ * ENVIRONMENT (tuning and test aids; read once per process unless noted):
  *   SVK_PDL=0          launch kernels without programmatic dependent launch;
  *   SVK_CHUNK_ROWS=n   node rows per CTA the strip kernels' wave sizing aims at
  *                      (default 64);
- *   SVK_POISON_HALO=1  NaN-fill rows beyond the halo after each exchange (tests).
+ *   SVK_POISON_HALO=1  NaN-fill rows beyond the halo after each exchange (tests);
+ *   SVK_SMALL_N=n      levels with N <= n below the finest run as one cluster launch
+ *                      (default 16; 0: every level as separate kernels) -- read at
+ *                      svk_create (results agree to rounding: same operators);
+ *   SVK_SMALL_CLUSTER=c  CTAs of that cluster (default 16, halved until the device
+ *                      can co-schedule it);
+ *   SVK_GRAPHS=0       replay no CUDA graphs (direct launches) inside svk_fgmres.
  * Compile time: -DSVK_STRIP_THREADS=64|128 (threads per strip CTA, default 64).
  */
 #ifndef SVK_H_
