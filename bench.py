@@ -15,8 +15,10 @@ reported as `setup_s`.
 value  = DOFs solved per second (whole job).
 sweep  = the finest-level Vanka sweeps inside the timed solves (CUDA events on the
          sweep stream, svk_set_profiling): DOF/s, algorithmic HBM GB/s, roofline.
-e2e    = the same solve through svk_solve_host with pinned HOST buffers (H2D of
-         b and x0, D2H of x inside the timed region).
+e2e    = the same solve from pinned HOST buffers through svk_solve_host_batch: a
+         stream of >= 4 problems, every step's H2D of b and x0 and D2H of x inside
+         the timed region, the copies of steps k+1 / k-1 overlapping the solve of
+         step k; e2e.serial = one svk_solve_host call per step (nothing overlapped).
 --impl reference  times the CPU oracle (oracle/, C++ + OpenMP, fp64) on a bounded
          sample of the same workload (a 512^2 solve per step, the cpu_baseline's size) on the host cores.
 Multi-GPU (N > 1): one process per GPU under torchrun (bench.py relaunches itself
@@ -372,6 +374,15 @@ def run_svk(args):
         xh = torch.empty_like(bh).pin_memory()
         bn, x0n, xn = bh.numpy(), x0h.numpy(), xh.numpy()
         S.solve_host(bn, x0n, rtol=args.rtol, x_host=xn)  # warm
+
+        def tmax_of(t):
+            if dist:
+                tt = torch.tensor([t], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            return t
+
+        # (1) one svk_solve_host call per step: copies in, solve, copy out, serially
         if dist:
             dist.barrier()
         te = []
@@ -379,15 +390,31 @@ def run_svk(args):
             t1 = time.perf_counter()
             _, repe = S.solve_host(bn, x0n, rtol=args.rtol, x_host=xn)
             te.append(time.perf_counter() - t1)
-        tmax = sum(te)
+        t_serial = tmax_of(sum(te))
+        # (2) svk_solve_host_batch over the steps as a stream of problems (own pinned
+        # input / output arrays per step): every step's H2D and D2H are made, the
+        # copies of steps k+1 / k-1 overlapping the solve of step k
+        kb = max(args.e2e_steps, 8)
+        bl = [torch.empty_like(bh).pin_memory().numpy() for _ in range(kb)]
+        x0l = [torch.empty_like(bh).pin_memory().numpy() for _ in range(kb)]
+        xl = [torch.empty_like(bh).pin_memory().numpy() for _ in range(kb)]
+        for a, c in zip(bl, x0l):
+            a[:] = bn
+            c[:] = x0n
         if dist:
-            tt = torch.tensor([tmax], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tmax = float(tt.item())
-        e2e = {"value": jobs * n_dof(N) * args.e2e_steps / tmax, "unit": "DOF/s",
+            dist.barrier()
+        t1 = time.perf_counter()
+        _, repb, _ = S.solve_host_batch(bl, x0l, rtol=args.rtol, x_hosts=xl)
+        t_batch = tmax_of(time.perf_counter() - t1)
+        assert all(r["iterations"] == repe["iterations"] for r in repb) and np.array_equal(xl[-1], xn)
+        e2e = {"value": jobs * n_dof(N) * kb / t_batch, "unit": "DOF/s",
                "h2d_bytes_per_step": world * 2 * n_dof(N) * 8, "d2h_bytes_per_step": world * n_dof(N) * 8,
-               "steps": args.e2e_steps, "ms_per_step": 1e3 * tmax / args.e2e_steps,
-               "api": "svk_solve_host (compact host arrays, pinned)"}
+               "steps": kb, "ms_per_step": 1e3 * t_batch / kb,
+               "api": "svk_solve_host_batch (a stream of %d problems from pinned compact host arrays; the H2D of "
+                      "step k+1 and the D2H of step k-1 overlap the solve of step k on two copy streams)" % kb,
+               "serial": {"value": jobs * n_dof(N) * args.e2e_steps / t_serial, "steps": args.e2e_steps,
+                          "ms_per_step": 1e3 * t_serial / args.e2e_steps,
+                          "api": "svk_solve_host per step (copies in, solve, copy out, nothing overlapped)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

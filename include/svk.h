@@ -348,6 +348,20 @@ int svk_fgmres(svk_ctx* ctx, const double* b, double* x, double rtol, int32_t ma
 int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, double* x_host, double rtol,
                    int32_t maxit, svk_report* rep, void* stream);
 
+/* Pipelined end-to-end solves of `count` independent problems from HOST buffers
+ * (b_host[k], x0_host[k] in, x_host[k] out; compact layout as svk_solve_host;
+ * pinned buffers let the copies run asynchronously): problem k is solved on
+ * `stream` (svk_fgmres) while the host->device copies of problem
+ * k+1 and the device->host copy of problem k-1 run on two library-owned copy
+ * streams (two device staging pairs, allocated on first use).  Every problem's
+ * copies are made; only their overlap with the solves differs from calling
+ * svk_solve_host `count` times, and the results are bitwise the same.  reps
+ * (optional, host) receives `count` reports.  Returns the largest per-problem
+ * status (SVK_OK or SVK_NOT_CONVERGED) or the first error (remaining problems
+ * are not solved).  Multi-GPU: as svk_solve_host, all ranks call together. */
+int svk_solve_host_batch(svk_ctx* ctx, int32_t count, const double* const* b_host, const double* const* x0_host,
+                         double* const* x_host, double rtol, int32_t maxit, svk_report* reps, void* stream);
+
 /* Introspection for tests: the dense inverse of patch group (cat_x, cat_y),
  * cat in {0: k=0, 1: k=1, 2: 2<=k<=N-2, 3: k=N-1, 4: k=N}, on `level`,
  * copied to host `out` (n*n doubles, row-major, n <= 51); *n receives the

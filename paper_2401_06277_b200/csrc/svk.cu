@@ -71,9 +71,17 @@ struct svk_ctx {
   double* d_part = nullptr;
   double* d_coef = nullptr;
   double* h_pin = nullptr;
+  double* h_pin_dev = nullptr;  // h_pin is mapped: the device address of the same memory
   int coef_cap = 0;
   double* d_hb = nullptr;  // e2e staging
   double* d_hx = nullptr;
+  // svk_solve_host_batch: a second staging pair and two copy streams + events
+  double* d_hb2 = nullptr;
+  double* d_hx2 = nullptr;
+  double* d_cin[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // compact staging: [pair][b, x0]
+  double* d_cout[2] = {nullptr, nullptr};                          // compact staging of x
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaEvent_t ev[6]{};
   int64_t launches = 0;
   // sweep profiling (svk_set_profiling / svk_sweep_stats)
@@ -830,6 +838,25 @@ int op_agglomerate(svk_ctx* ctx, int l, double* rc, cudaStream_t s) {
 // agglomeration level the restricted residual is assembled on every rank by an
 // all-reduce of the disjoint, zero-padded slab pieces; the coarser levels then
 // run redundantly (replicated) on every rank.
+// compact [u_x lat^2, u_y lat^2, p (N+1)^2] <-> pitched finest-level layout, on the device
+// (svk_solve_host_batch: the host copies stay 1D and contiguous)
+template <bool TO_PITCHED>
+__global__ void k_repitch(LevelGeom g, const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t nv = (int64_t)g.lat * g.lat, np = (int64_t)(g.N + 1) * (g.N + 1);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 2 * nv + np; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o;
+    if (q < 2 * nv) {
+      const int64_t qq = q < nv ? q : q - nv;
+      o = (q < nv ? g.oux : g.ouy) + (qq / g.lat) * g.pu + qq % g.lat;
+    } else {
+      const int64_t qq = q - 2 * nv;
+      o = g.op + (qq / (g.N + 1)) * g.pp + qq % (g.N + 1);
+    }
+    if (TO_PITCHED) dst[o] = src[q];
+    else dst[q] = src[o];
+  }
+}
+
 // Which coarse levels run in the one-launch V-cycle, and on how many CTAs.
 // SVK_SMALL_N (default 16, measured best: 4096^2 V-cycle 5378 -> 5341 us, 1024^2
 // 859 -> 813 us; at 32 / 64 the grid-stride phases of the larger levels cost
@@ -1106,9 +1133,25 @@ int ensure_coef(svk_ctx* ctx, int need) {
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   CK(cudaMalloc(&ctx->d_coef, cap * sizeof(double)));
   CK(cudaMemset(ctx->d_coef, 0, cap * sizeof(double)));  // read back in whole blocks: keep it defined
-  CK(cudaMallocHost(&ctx->h_pin, cap * sizeof(double)));
+  CK(cudaHostAlloc(&ctx->h_pin, cap * sizeof(double), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(&ctx->h_pin_dev, ctx->h_pin, 0));
   std::memset(ctx->h_pin, 0, cap * sizeof(double));
   ctx->coef_cap = cap;
+  return SVK_OK;
+}
+// Krylov coefficients back to the host: a one-CTA kernel stores them straight into the
+// mapped pinned buffer (posted PCIe writes) instead of a cudaMemcpyAsync D2H, which a
+// copy engine would queue behind any large device-to-host transfer in flight (the
+// pipelined svk_solve_host_batch copies solution k-1 out while solving problem k: a
+// per-iteration D2H readback then waits for it, +10% solve time).
+__global__ void k_to_mapped(const double* __restrict__ src, double* __restrict__ dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+int readback(svk_ctx* ctx, const double* src, int n, cudaStream_t s) {
+  k_to_mapped<<<1, 128, 0, s>>>(src, ctx->h_pin_dev, n);
+  CKL();
+  ctx->launches++;
+  CK(cudaStreamSynchronize(s));
   return SVK_OK;
 }
 // ---------------------------------------------------------------------------
@@ -1156,8 +1199,7 @@ int cgs_update(svk_ctx* ctx, const double* const* dV, int m, int coff, const dou
 // |v| on the host (owned segments, all-reduced)
 int host_norm(svk_ctx* ctx, const double* v, const Seg3& S, double* out, cudaStream_t s) {
   TRY(cgs_dots(ctx, &v, 1, v, S, 0, s));
-  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  TRY(readback(ctx, ctx->d_coef, 1, s));
   *out = std::sqrt(std::max(ctx->h_pin[0], 0.0));
   return SVK_OK;
 }
@@ -1196,8 +1238,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
   TRY(op_halo(ctx, L, x, s));
   TRY(op_residual(ctx, L, x, b, ctx->V[0], s));
   TRY(cgs_dots(ctx, (const double* const*)ctx->V.data(), 1, ctx->V[0], S, onrm, s));
-  CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef + onrm, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  TRY(readback(ctx, ctx->d_coef + onrm, 1, s));
   const double beta = std::sqrt(std::max(ctx->h_pin[0], 0.0));
   if (hist) hist[0] = 1.0;
   if (!std::isfinite(beta)) {
@@ -1240,8 +1281,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
       CKL();
       TRY(cgs_update(ctx, hV, m, o1, ctx->d_w, ctx->V[j + 1], n, S, onrm, s));
       CK(cudaEventRecord(ctx->ev[2], s));
-      CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      TRY(readback(ctx, ctx->d_coef, (onrm + 1), s));
       TRY(harvest_graph_prof(ctx));
       if (ctx->tr && ctx->tr->async_error(ctx->err) != 0) return SVK_ERR_NCCL;  // polled once per iteration
       float a01 = 0, a12 = 0;
@@ -1258,8 +1298,7 @@ int fgmres_impl(svk_ctx* ctx, const double* b, double* x, double rtol, int maxit
         CKL();
         TRY(cgs_update(ctx, hV, m, o2, ctx->V[j + 1], ctx->V[j + 1], n, S, onrm, s));
         CK(cudaEventRecord(ctx->ev[4], s));
-        CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_coef, (onrm + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        TRY(readback(ctx, ctx->d_coef, (onrm + 1), s));
         float a34 = 0;
         cudaEventElapsedTime(&a34, ctx->ev[3], ctx->ev[4]);
         to += a34 * 1e-3;
@@ -1393,6 +1432,18 @@ int free_ctx(svk_ctx* ctx) {
   F(ctx->d_coef);
   F(ctx->d_hb);
   F(ctx->d_hx);
+  F(ctx->d_hb2);
+  F(ctx->d_hx2);
+  for (int q = 0; q < 2; ++q) {
+    F(ctx->d_cin[q][0]);
+    F(ctx->d_cin[q][1]);
+    F(ctx->d_cout[q]);
+  }
+  for (cudaEvent_t* e : {ctx->ev_in, ctx->ev_solved, ctx->ev_out})
+    for (int k = 0; k < 2; ++k)
+      if (e[k]) cudaEventDestroy(e[k]);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   for (auto e : ctx->prof_ev) cudaEventDestroy(e);
   for (auto& gr : ctx->graphs) {
@@ -1972,6 +2023,90 @@ int svk_solve_host(svk_ctx* ctx, const double* b_host, const double* x0_host, do
                          cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return st;
+  });
+}
+
+int svk_solve_host_batch(svk_ctx* ctx, int32_t count, const double* const* b_host, const double* const* x0_host,
+                         double* const* x_host, double rtol, int32_t maxit, svk_report* reps, void* stream) {
+  return guarded(ctx, [&]() -> int {
+    if (count < 1 || !b_host || !x0_host || !x_host) return SVK_ERR_INVALID;
+    if (maxit < 1 || !(rtol >= 0)) {
+      ctx->err = "maxit < 1 or rtol not >= 0";
+      return SVK_ERR_INVALID;
+    }
+    for (int k = 0; k < count; ++k) {
+      if (!b_host[k] || !x0_host[k] || !x_host[k]) return SVK_ERR_INVALID;
+      if (x_host[k] == b_host[k] || x_host[k] == x0_host[k]) {
+        ctx->err = "x_host aliases an input";
+        return SVK_ERR_INVALID;
+      }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const LevelGeom& g = ctx->g.back();
+    if (!ctx->d_hb) TRY(alloc_vec(ctx, &ctx->d_hb, g.len));
+    if (!ctx->d_hx) TRY(alloc_vec(ctx, &ctx->d_hx, g.len));
+    if (!ctx->d_hb2) TRY(alloc_vec(ctx, &ctx->d_hb2, g.len));
+    if (!ctx->d_hx2) TRY(alloc_vec(ctx, &ctx->d_hx2, g.len));
+    const int64_t nc = 2 * (int64_t)g.lat * g.lat + (int64_t)(g.N + 1) * (g.N + 1);  // compact length
+    for (int q = 0; q < 2; ++q) {
+      if (!ctx->d_cin[q][0]) TRY(alloc_vec(ctx, &ctx->d_cin[q][0], nc));
+      if (!ctx->d_cin[q][1]) TRY(alloc_vec(ctx, &ctx->d_cin[q][1], nc));
+      if (!ctx->d_cout[q]) TRY(alloc_vec(ctx, &ctx->d_cout[q], nc));
+    }
+    const size_t cbytes = (size_t)nc * sizeof(double);
+    const dim3 rgrid((unsigned)std::min<int64_t>((nc + 255) / 256, 8 * ctx->nsm)), rblk(256);
+    if (!ctx->s_in) {
+      CK(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {ctx->ev_in, ctx->ev_solved, ctx->ev_out})
+        for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&e[k], cudaEventDisableTiming));
+    }
+    double* hb[2] = {ctx->d_hb, ctx->d_hb2};
+    double* hx[2] = {ctx->d_hx, ctx->d_hx2};
+    // the copy streams start after everything already queued on `stream`
+    CK(cudaEventRecord(ctx->ev_solved[1], s));
+    CK(cudaStreamWaitEvent(ctx->s_in, ctx->ev_solved[1], 0));
+    CK(cudaStreamWaitEvent(ctx->s_out, ctx->ev_solved[1], 0));
+    auto stage_in = [&](int k) -> int {  // problem k into staging pair k % 2 (after its previous D2H)
+      const int q = k & 1;
+      if (k >= 2) CK(cudaStreamWaitEvent(ctx->s_in, ctx->ev_solved[q], 0));  // staging pair q is free again
+      CK(cudaMemcpyAsync(ctx->d_cin[q][0], b_host[k], cbytes, cudaMemcpyHostToDevice, ctx->s_in));
+      CK(cudaMemcpyAsync(ctx->d_cin[q][1], x0_host[k], cbytes, cudaMemcpyHostToDevice, ctx->s_in));
+      CK(cudaEventRecord(ctx->ev_in[q], ctx->s_in));
+      return SVK_OK;
+    };
+    TRY(stage_in(0));
+    int worst = SVK_OK;
+    for (int k = 0; k < count; ++k) {
+      const int q = k & 1;
+      if (k + 1 < count) TRY(stage_in(k + 1));  // overlaps the solve of problem k
+      CK(cudaStreamWaitEvent(s, ctx->ev_in[q], 0));
+      k_repitch<true><<<rgrid, rblk, 0, s>>>(g, ctx->d_cin[q][0], hb[q]);
+      k_repitch<true><<<rgrid, rblk, 0, s>>>(g, ctx->d_cin[q][1], hx[q]);
+      CKL();
+      const int st = fgmres_impl(ctx, hb[q], hx[q], rtol, maxit, nullptr, reps ? &reps[k] : nullptr, s);
+      if (st < 0) {
+        cudaStreamSynchronize(ctx->s_in);
+        cudaStreamSynchronize(ctx->s_out);
+        return st;
+      }
+      if (st > worst) worst = st;
+      if (ctx->tr) {  // assemble the full solution on every rank
+        TRY(op_zero_unowned(ctx, ctx->nlev - 1, hx[q], s));
+        TRY(op_allreduce(ctx, hx[q], g.len, s));
+      }
+      if (k >= 2) CK(cudaStreamWaitEvent(s, ctx->ev_out[q], 0));  // D2H of problem k-2 has left d_cout[q]
+      k_repitch<false><<<rgrid, rblk, 0, s>>>(g, hx[q], ctx->d_cout[q]);
+      CKL();
+      ctx->launches += 3;
+      CK(cudaEventRecord(ctx->ev_solved[q], s));
+      CK(cudaStreamWaitEvent(ctx->s_out, ctx->ev_solved[q], 0));
+      CK(cudaMemcpyAsync(x_host[k], ctx->d_cout[q], cbytes, cudaMemcpyDeviceToHost, ctx->s_out));  // overlaps solve k+1
+      CK(cudaEventRecord(ctx->ev_out[q], ctx->s_out));
+    }
+    CK(cudaStreamSynchronize(ctx->s_out));
+    CK(cudaStreamSynchronize(ctx->s_in));
+    return worst;
   });
 }
 

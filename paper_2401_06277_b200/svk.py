@@ -108,6 +108,8 @@ EXPORTS = {
                              C.POINTER(Report), C.c_void_p]),
     "svk_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                                  C.POINTER(Report), C.c_void_p]),
+    "svk_solve_host_batch": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_void_p), C.c_double, C.c_int32, C.POINTER(Report), C.c_void_p]),
     "svk_patch_inverse": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
     "svk_validate_patches": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "svk_device_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
@@ -394,19 +396,43 @@ class Solver:
         d["status"] = st
         return d, hist[: rep.iterations + 1].copy()
 
+    def _host(self, a, name, writable=False):
+        li = self.info[self.fine]
+        n = 2 * li.lat * li.lat + (li.N + 1) ** 2
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+                and a.ndim == 1 and a.size == n and (a.flags["WRITEABLE"] or not writable)):
+            raise SvkError("%s: expected a C-contiguous%s float64 host array of %d elements"
+                           % (name, " writable" if writable else "", n))
+        return a
+
+    def solve_host_batch(self, b_hosts, x0_hosts, rtol: float = 1e-10, maxit: int = 200, x_hosts=None):
+        """Pipelined end-to-end solves of several problems from host arrays
+        (svk_solve_host_batch): the copies of problems k+1 / k-1 overlap the solve of
+        problem k.  Returns (list of x arrays, list of report dicts, status)."""
+        k = len(b_hosts)
+        if k < 1 or len(x0_hosts) != k or (x_hosts is not None and len(x_hosts) != k):
+            raise SvkError("b_hosts / x0_hosts / x_hosts: equal non-zero lengths expected")
+        bs = [self._host(a, "b_hosts[%d]" % i) for i, a in enumerate(b_hosts)]
+        x0s = [self._host(a, "x0_hosts[%d]" % i) for i, a in enumerate(x0_hosts)]
+        xs = ([np.empty_like(bs[0]) for _ in range(k)] if x_hosts is None
+              else [self._host(a, "x_hosts[%d]" % i, writable=True) for i, a in enumerate(x_hosts)])
+        for i, x in enumerate(xs):
+            if np.shares_memory(x, bs[i]) or np.shares_memory(x, x0s[i]):
+                raise SvkError("x_hosts[%d] aliases an input" % i)
+        ptrs = lambda arrs: (C.c_void_p * k)(*[a.ctypes.data for a in arrs])
+        reps = (Report * k)()
+        st = self._chk(self.lib.svk_solve_host_batch(self._h, k, ptrs(bs), ptrs(x0s), ptrs(xs), rtol, maxit,
+                                                     reps, self._stream()))
+        out = []
+        for r in reps:
+            d = r.as_dict()
+            out.append(d)
+        return xs, out, st
+
     def solve_host(self, b_host: np.ndarray, x0_host: np.ndarray, rtol: float = 1e-10, maxit: int = 200,
                    x_host: np.ndarray | None = None):
         """End-to-end solve from host arrays in the compact layout (svk_solve_host)."""
-        li = self.info[self.fine]
-        n = 2 * li.lat * li.lat + (li.N + 1) ** 2
-
-        def host(a, name, writable=False):
-            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
-                    and a.ndim == 1 and a.size == n and (a.flags["WRITEABLE"] or not writable)):
-                raise SvkError("%s: expected a C-contiguous%s float64 host array of %d elements"
-                               % (name, " writable" if writable else "", n))
-            return a
-
+        host = self._host
         b_host, x0_host = host(b_host, "b_host"), host(x0_host, "x0_host")
         x_host = np.empty_like(b_host) if x_host is None else host(x_host, "x_host", writable=True)
         if np.shares_memory(x_host, b_host) or np.shares_memory(x_host, x0_host):
