@@ -215,6 +215,26 @@ def test_dist_solve_host(gpu, poison):
         S.close()
 
 
+def test_dist_solve_host_batch(gpu, poison):
+    # svk_solve_host_batch on 2 emulated ranks: every rank assembles every solution,
+    # bitwise the per-problem svk_solve_host results
+    P, N, agg = 2, 64, 8
+    O = oracle.Oracle(N)
+    probs = [O.problem(oracle.CAVITY), O.problem(oracle.MMS_PAPER)]
+    Ss = make_solvers(P, N, agg)
+    single = run_ranks(P, lambda r: [Ss[r].solve_host(b, x0, rtol=1e-10, maxit=100) for b, x0 in probs])
+    batch = run_ranks(P, lambda r: Ss[r].solve_host_batch([p[0] for p in probs], [p[1] for p in probs],
+                                                          rtol=1e-10, maxit=100))
+    for r in range(P):
+        xs, reps, st = batch[r]
+        assert st == 0
+        for (x1, r1), x2, r2 in zip(single[r], xs, reps):
+            assert np.array_equal(x1, x2) and r1["iterations"] == r2["iterations"]
+    assert all(np.array_equal(a, b) for a, b in zip(batch[0][0], batch[1][0]))
+    for S in Ss:
+        S.close()
+
+
 def test_dist_config_errors(gpu):
     from paper_2401_06277_b200 import Solver, SvkError
     with pytest.raises(SvkError):
