@@ -326,24 +326,9 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
   // Rows a slab-local vector does not hold are never read by the band's stencils
   // (the stencils of band rows outside the slab's patch rows are skipped below).
   const int jlo = 2 * (g.r0 - 1) - 4, jhi = 2 * g.r1 + 4;
-  // ---- phase 0: every global load of the tile ----
-  for (int q = threadIdx.x; q < kGroupStride; q += blockDim.x) Ai[q] = A[q];
-  if (x) {
-    for (int q = threadIdx.x; q < NXS + NPS; q += blockDim.x) {
-      double v = 0.0;
-      if (q < NXS) {
-        const int comp = q / (9 * kBdStA), rem = q % (9 * kBdStA), ac = rem / kBdStA, al = rem % kBdStA;
-        const int i = i0 - 2 + (tl.dx ? al : ac), j = j0 - 2 + (tl.dx ? ac : al);
-        if (i >= 0 && j >= 0 && i < lat && j < lat && j >= jlo && j <= jhi)
-          v = x[(comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i];
-      } else {
-        const int r = q - NXS, ac = r / (T + 4), al = r % (T + 4);
-        const int kx = tl.kx - 2 + (tl.dx ? al : ac), ky = tl.ky - 2 + (tl.dx ? ac : al);
-        if (kx >= 0 && ky >= 0 && kx <= N && ky <= N && 2 * ky >= jlo && 2 * ky <= jhi) v = x[p_at(g, kx, ky)];
-      }
-      xs[q] = v;
-    }
-  }
+  // ---- phase 0: every global load of the tile, all in flight at once (registers
+  //      first, then shared memory: loop-carried load->store pairs would expose one
+  //      L2 round trip per iteration) ----
   // b on the band (0 where the residual is not formed: Dirichlet / outside / beyond the slab)
   auto band_ij = [&](int q, int& comp, int& i, int& j, bool& ok) {
     comp = q / (5 * kBdBandW);
@@ -355,7 +340,34 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
     const bool jslab = j >= 2 * (g.r0 - 1) - 2 && j <= 2 * g.r1 + 2;
     ok = al < nalong && jslab && i >= 1 && j >= 1 && i <= lat - 2 && j <= lat - 2;
   };
-  for (int q = threadIdx.x; q < NBAND + T; q += blockDim.x) {
+  constexpr int NA = (kGroupStride + kBdThreads - 1) / kBdThreads;
+  constexpr int NX = (NXS + NPS + kBdThreads - 1) / kBdThreads;
+  constexpr int NB = (NBAND + T + kBdThreads - 1) / kBdThreads;
+  double va[NA], vx[NX], vb[NB];
+#pragma unroll
+  for (int u = 0; u < NA; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
+    va[u] = q < kGroupStride ? __ldg(A + q) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
+    double v = 0.0;
+    if (x && q < NXS) {
+      const int comp = q / (9 * kBdStA), rem = q % (9 * kBdStA), ac = rem / kBdStA, al = rem % kBdStA;
+      const int i = i0 - 2 + (tl.dx ? al : ac), j = j0 - 2 + (tl.dx ? ac : al);
+      if (i >= 0 && j >= 0 && i < lat && j < lat && j >= jlo && j <= jhi)
+        v = x[(comp ? g.ouy : g.oux) + (int64_t)j * g.pu + i];
+    } else if (x && q < NXS + NPS) {
+      const int r = q - NXS, ac = r / (T + 4), al = r % (T + 4);
+      const int kx = tl.kx - 2 + (tl.dx ? al : ac), ky = tl.ky - 2 + (tl.dx ? ac : al);
+      if (kx >= 0 && ky >= 0 && kx <= N && ky <= N && 2 * ky >= jlo && 2 * ky <= jhi) v = x[p_at(g, kx, ky)];
+    }
+    vx[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
     double v = 0.0;
     if (q < NBAND) {
       int comp, i, j;
@@ -366,7 +378,22 @@ __global__ void __launch_bounds__(kBdThreads, SVK_BD_MINB) k_boundary_patches(Le
       const int pi = q - NBAND;
       v = b[p_at(g, tl.kx + pi * tl.dx, tl.ky + pi * tl.dy)];
     }
-    band[q] = v;
+    vb[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < NA; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
+    if (q < kGroupStride) Ai[q] = va[u];
+  }
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
+    if (x && q < NXS + NPS) xs[q] = vx[u];
+  }
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int q = threadIdx.x + u * kBdThreads;
+    if (q < NBAND + T) band[q] = vb[u];
   }
   // ---- phase 1: r = b - A x on the band ----
   if (x) {
