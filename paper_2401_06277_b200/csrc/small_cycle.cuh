@@ -521,7 +521,17 @@ __global__ void __launch_bounds__(kScThreads, 1) k_small_cycle(const __grid_cons
       const int n = A.cni + 1;
       for (int rr = T.gw; rr < A.cni; rr += T.nw) {  // one warp per row (k_coarse_apply)
         double s = 0.0;
-        for (int c = T.lane; c < A.cni; c += 32) s = fma(A.cmat[(int64_t)rr * n + c], LDX(L.b + A.cidx[c]), s);
+        // the level-0 system has 98 + 25 = 123 unknowns: 4 columns per lane, loads first
+        double mv[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = T.lane + 32 * u, cc = min(c, A.cni - 1);
+          mv[u] = c < A.cni ? A.cmat[(int64_t)rr * n + cc] : 0.0;
+          bv[u] = LDX(L.b + A.cidx[cc]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = fma(mv[u], bv[u], s);
+        for (int c = T.lane + 128; c < A.cni; c += 32) s = fma(A.cmat[(int64_t)rr * n + c], LDX(L.b + A.cidx[c]), s);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (T.lane == 0) L.x[A.cidx[rr]] = s;
