@@ -71,7 +71,8 @@
  *                      (default 16; 0: every level as separate kernels) -- read at
  *                      svk_create (results agree to rounding: same operators);
  *   SVK_SMALL_CLUSTER=c  CTAs of that cluster (default 16, halved until the device
- *                      can co-schedule it);
+ *                      can co-schedule it; an explicit c is used as given, and a
+ *                      launch the device rejects falls back to separate kernels);
  *   SVK_GRAPHS=0       replay no CUDA graphs (direct launches) inside svk_fgmres.
  * Compile time: -DSVK_STRIP_THREADS=64|128 (threads per strip CTA, default 64).
  */

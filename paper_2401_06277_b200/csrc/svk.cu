@@ -874,9 +874,9 @@ int setup_small_cycle(svk_ctx* ctx) {
     if (ctx->g[l].N <= lc && !dist_level(ctx, l)) top = l;
   if (top < 1) return SVK_OK;
   CK(cudaFuncSetAttribute(k_small_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  const char* ce = std::getenv("SVK_SMALL_CLUSTER");
+  const char* ce = std::getenv("SVK_SMALL_CLUSTER");  // taken as given (no occupancy check): a test hook
   int cl = ce ? std::atoi(ce) : 16;
-  for (; cl >= 1; cl /= 2) {
+  for (; cl >= 1 && !ce; cl /= 2) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)cl);
     cfg.blockDim = dim3(kScThreads);
@@ -913,6 +913,7 @@ int setup_small_cycle(svk_ctx* ctx) {
   return SVK_OK;
 }
 
+int op_mg(svk_ctx* ctx, int l, const double* b, double* x, bool x_zero, cudaStream_t s);
 // MG(l) from x = 0 on the levels l .. 0 (alg:mg) as ONE cluster launch
 // (small_cycle.cuh): same steps and operators as the per-kernel recursion below.
 int op_small_cycle(svk_ctx* ctx, int l, const double* b, double* x, cudaStream_t s) {
@@ -958,7 +959,19 @@ int op_small_cycle(svk_ctx* ctx, int l, const double* b, double* x, cudaStream_t
     if (!stamps) CK(cudaMallocManaged(&stamps, 4096 * sizeof(unsigned long long)));
     a.stamps = stamps;
   }
-  CK(cudaLaunchKernelEx(&cfg, k_small_cycle, a));
+  if (const cudaError_t le = cudaLaunchKernelEx(&cfg, k_small_cycle, a); le != cudaSuccess) {
+    // a cluster the device cannot place right now (e.g. a partitioned GPU): outside a
+    // stream capture, fall back to the per-kernel recursion for good
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone) {
+      ctx->err = std::string("coarse cycle launch: ") + cudaGetErrorString(le);
+      return SVK_ERR_CUDA;
+    }
+    cudaGetLastError();
+    ctx->sc_top = 0;
+    return op_mg(ctx, l, b, x, true, s);
+  }
   if (a.stamps) {
     CK(cudaStreamSynchronize(s));
     std::string o = "[small-cycle us]";

@@ -61,3 +61,24 @@ def test_small_cycle_fgmres_iterations(gpu):
         rep, _ = S.fgmres(bb, x0, rtol=1e-10, maxit=60)
         S.its = rep["iterations"]
     assert abs(A.its - B.its) <= 1
+
+
+def test_small_cycle_launch_failure_falls_back(gpu):
+    # a cluster size the device cannot launch (32 > 16): the first launch fails, the
+    # context switches to the per-kernel recursion, results unchanged
+    old = os.environ.get("SVK_SMALL_CLUSTER")
+    os.environ["SVK_SMALL_CLUSTER"] = "32"
+    try:
+        A = _solver(64, 16)
+    finally:
+        if old is None:
+            del os.environ["SVK_SMALL_CLUSTER"]
+        else:
+            os.environ["SVK_SMALL_CLUSTER"] = old
+    B = _solver(64, 0)
+    O = oracle.Oracle(64)
+    b = svk_inputs.random_vector(64, 11)
+    b[O.dirichlet(O.fine)] = 0.0
+    za = A.to_compact(A.vcycle(A.from_compact(b))).cpu().numpy()
+    zb = B.to_compact(B.vcycle(B.from_compact(b))).cpu().numpy()
+    assert np.array_equal(za, zb)
