@@ -82,3 +82,19 @@ def test_small_cycle_launch_failure_falls_back(gpu):
     za = A.to_compact(A.vcycle(A.from_compact(b))).cpu().numpy()
     zb = B.to_compact(B.vcycle(B.from_compact(b))).cpu().numpy()
     assert np.array_equal(za, zb)
+
+
+@pytest.mark.parametrize("nu", [(0, 1), (1, 0), (3, 1)])
+def test_small_cycle_smoothing_counts(gpu, nu):
+    # V(nu1, nu2) with the coarse levels in one launch, against the per-kernel path
+    # and the oracle (alg:mg with nu1 pre- and nu2 post-smoothing sweeps)
+    N = 64
+    A = _solver(N, 16, nu_pre=nu[0], nu_post=nu[1])
+    B = _solver(N, 0, nu_pre=nu[0], nu_post=nu[1])
+    O = oracle.Oracle(N, nu1=nu[0], nu2=nu[1])
+    b = svk_inputs.random_vector(N, 13)
+    b[O.dirichlet(O.fine)] = 0.0
+    za = A.to_compact(A.vcycle(A.from_compact(b))).cpu().numpy()
+    zb = B.to_compact(B.vcycle(B.from_compact(b))).cpu().numpy()
+    assert rel(za, zb) <= 1e-13
+    assert rel(za, O.vcycle(b)) <= 1e-12
