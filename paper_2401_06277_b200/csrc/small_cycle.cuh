@@ -18,10 +18,15 @@
 // unfused form of the paper's kernel split (alg:vk_kernels):
 //   residual r = b - A x (masked, k_residual's stencils)            [phase]
 //   patch solves delta_i = A_i^{-1} V_i r by the group's dense inverse on the
-//     FP64 tensor path (one warp per tile of <= 16 patches of one group, as
-//     k_boundary_patches does for the boundary patches)              [phase]
+//     FP64 tensor path: one warp per (tile of <= 16 patches of one group, n8 tile
+//     of the 51 slots), 13 k-steps of mma.sync.m8n8k4.f64 -- a warp issues a DMMA
+//     only every ~25-35 cycles, so a tile's 7 slot tiles go to 7 warps  [phase]
 //   x_out = x_in + W sum_i V_i^T delta_i (owner gathers, fixed order) [phase]
 //   restriction r_c = P^T r, prolongation x += P e_c, level-0 min-norm solve.
+// Point phases: one warp per lattice / pressure row (no 64-bit index division),
+// every load of a point issued before its arithmetic; the stencil rows the lanes
+// index by their own parity come from shared memory (divergent __constant__ reads
+// serialise).  SVK_DEBUG_SMALL=2 (with SVK_GRAPHS=0) prints %globaltimer per phase.
 // Data produced inside the launch is ordered by the barrier's release/acquire
 // (the acquire invalidates the SM's L1), so phases read it with plain loads.
 #pragma once
